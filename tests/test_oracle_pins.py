@@ -1,0 +1,483 @@
+"""Pins of the CPU oracle against what the paper and mathematics fix (no GPU).
+
+Every test here checks oracle/ against something other than itself: the worked
+examples in tests/golden/spec_examples.json, closed forms of Eqs. (2)-(6), invariants,
+a pixel-centric brute force (oracle/brute.py, O0) and finite differences.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import brute, oracle
+from synth import scenes
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+
+
+def unit_cam(W=64, H=64, f=1.0, cx=0.0, cy=0.0):
+    return scenes.Camera(fx=f, fy=f, cx=cx, cy=cy, f=f, R=np.eye(3, dtype=np.float32),
+                         t=np.zeros(3, np.float32), width=W, height=H)
+
+
+def point_scene(cam, pts, sizes, alpha=None, desc=None, F=1):
+    """Points given in pixel coordinates (u, v, z) with screen size s (fx == fy)."""
+    pts = np.asarray(pts, np.float64)
+    n = pts.shape[0]
+    pos = np.stack([(pts[:, 0] - cam.cx) * pts[:, 2] / cam.fx,
+                    (pts[:, 1] - cam.cy) * pts[:, 2] / cam.fy, pts[:, 2]], 1)
+    sw = np.asarray(sizes, np.float64) * pts[:, 2] / cam.f
+    alpha = np.ones(n) if alpha is None else np.asarray(alpha, np.float64)
+    desc = np.ones((n, F)) if desc is None else np.asarray(desc, np.float64).reshape(n, -1)
+    return pos.astype(np.float32), sw.astype(np.float32), alpha.astype(np.float32), desc.astype(np.float32)
+
+
+# ------------------------------------------------------------------ projection (P1)
+
+def test_projection_spec_examples():
+    for ex in GOLD["projection"]:
+        cam = scenes.Camera(fx=ex["fx"], fy=ex["fy"], cx=ex["cx"], cy=ex["cy"], f=ex["fx"],
+                            R=np.eye(3, dtype=np.float32), t=np.zeros(3, np.float32), width=100, height=100)
+        proj, level, _ = oracle.project(cam, 4, np.array([ex["point"]], np.float32), np.array([0.01], np.float32))
+        if ex.get("expect_culled"):
+            assert level[0] == -1 and np.isnan(proj[0]).all(), ex["cite"]
+        else:
+            assert np.array_equal(proj[0, :3], np.array(ex["expect_xyz"], np.float32)), ex["cite"]
+
+
+@pytest.mark.parametrize("seed", range(5))
+def test_projection_vs_homogeneous_4x4(seed):
+    """P1: fp64 4x4 homogeneous projection K [R|t] (a different formulation) within 1e-6."""
+    sc = scenes.tiny_scene(seed, n=300)
+    cam = sc.cams[0]
+    proj, level, _ = oracle.project(cam, sc.n_layers, sc.pos, sc.sw)
+    fx, fy, cx, cy, f = (float(np.float32(v)) for v in (cam.fx, cam.fy, cam.cx, cam.cy, cam.f))
+    K = np.array([[fx, 0, cx, 0], [0, fy, cy, 0], [0, 0, 1, 0], [0, 0, 0, 1]], np.float64)
+    E = np.eye(4)
+    E[:3, :3] = cam.R.astype(np.float64)
+    E[:3, 3] = cam.t.astype(np.float64)
+    X = np.concatenate([sc.pos.astype(np.float64), np.ones((sc.n, 1))], 1)
+    H = (K @ E @ X.T).T
+    z = H[:, 2]
+    uv = H[:, :2] / z[:, None]
+    s = f * sc.sw.astype(np.float64) / z
+    vis = level >= 0
+    assert vis.sum() > 0
+    assert np.array_equal(vis, z > cam.near)
+    scale = np.maximum(np.abs(uv[vis]), 1.0)
+    assert (np.abs(proj[vis, :2] - uv[vis]) / scale).max() < 1e-5 * 64   # fp32 vs fp64, |uv| <~ 64
+    assert (np.abs(proj[vis, 2] - z[vis]) / np.abs(z[vis])).max() < 1e-6
+    assert (np.abs(proj[vis, 3] - s[vis]) / np.maximum(s[vis], 1e-30)).max() < 1e-6
+    # the fp64 build of the oracle agrees with the 4x4 form to 1e-12
+    p64, _, _ = oracle.project(cam, sc.n_layers, sc.pos, sc.sw, real="double")
+    assert (np.abs(p64[vis, :2] - uv[vis]) / scale).max() < 1e-12
+    assert (np.abs(p64[vis, 3] - s[vis]) / np.maximum(s[vis], 1e-30)).max() < 1e-12
+
+
+def test_screen_size_examples():
+    """P2: Eq. (2).  Evaluated in the fp64 build (inputs exact in fp32 where
+    dyadic); doubling z halves s exactly in the fp32 build for dyadic inputs."""
+    for ex in GOLD["screen_size"]:
+        cam = unit_cam(f=ex["f"])
+        proj, _, _ = oracle.project(cam, 4, np.array([[0, 0, ex["z"]]], np.float32),
+                                    np.array([ex["sw"]], np.float32), real="double")
+        assert abs(proj[0, 3] - ex["s"]) < 1e-7 * ex["s"], ex["cite"]
+    cam = unit_cam(f=512.0)
+    sw = np.array([0.03125, 0.03125], np.float32)
+    proj, _, _ = oracle.project(cam, 4, np.array([[0, 0, 2.0], [0, 0, 4.0]], np.float32), sw)
+    assert proj[1, 3] * 2 == proj[0, 3] == 8.0
+
+
+# ------------------------------------------------------------------ layers (P3)
+
+def levels_for(s, n_layers, real="float"):
+    s = np.asarray(s, np.float32)
+    cam = unit_cam()
+    pos = np.tile(np.array([[0, 0, 1.0]], np.float32), (s.size, 1))
+    proj, level, iota = oracle.project(cam, n_layers, pos, s, real=real)
+    assert np.array_equal(proj[:, 3], s.astype(proj.dtype))          # s = (1 * s_w) / 1 exactly
+    return level, iota
+
+
+def decode(code):
+    lo = code & 0x0F
+    return [lo, lo + 1] if code & 0x10 else [lo]
+
+
+def test_layer_spec_examples():
+    for ex in GOLD["layers"]:
+        level, iota = levels_for([ex["s"]], ex["n_layers"])
+        assert decode(int(level[0])) == ex["layers"], ex["cite"]
+        assert list(iota[0, :len(ex["layers"])]) == ex["iota"], ex["cite"]
+
+
+def test_power_of_two_lands_wholly_in_layer_k():
+    """North star: a point whose size is exactly 2^k lands wholly in layer k (Q2)."""
+    n = 8
+    ks = np.arange(0, n - 1)
+    level, iota = levels_for(2.0 ** ks, n)
+    for k, c, io in zip(ks, level, iota):
+        assert c == k and io[0] == 1.0 and io[1] == 0.0
+    level, iota = levels_for([2.0 ** (n - 1), 2.0 ** (n + 3)], n)   # clamp (Q5)
+    assert list(level) == [0x40 | (n - 1)] * 2 and list(iota[:, 0]) == [1.0, 1.0]
+
+
+def test_level_sweep_matches_eq4_in_fp64():
+    """P3: for s >= 1, iota from the oracle is bit-equal to Eq. (4) as written,
+    1 - |s - s_i| / (2^Lup - 2^Llo), evaluated in fp64.  Random fp32 values plus every
+    power-of-two neighbourhood; s < 1 (eps branch) within 1 ulp of fp64."""
+    n = 9
+    rng = np.random.default_rng(0)
+    bits = rng.integers(np.float32(1.0).view(np.int32), np.float32(256.0).view(np.int32), 400_000)
+    s = bits.astype(np.int32).view(np.float32)
+    edges = []
+    for k in range(0, 9):
+        b = np.float32(2.0 ** k).view(np.int32)
+        edges.append(np.arange(b - 64, b + 64, dtype=np.int32).view(np.float32))
+    s = np.concatenate([s] + edges)
+    s = s[(s >= 1) & (s < 2.0 ** (n - 1))]
+    level, iota = levels_for(s, n)
+    s64 = s.astype(np.float64)
+    Llo = np.floor(np.log2(s64)).astype(np.int64)
+    Lup = np.ceil(np.log2(s64)).astype(np.int64)
+    two = Lup != Llo
+    assert np.array_equal((level & 0x10) != 0, two)
+    assert np.array_equal(level & 0x0F, Llo)
+    den = 2.0 ** Lup[two] - 2.0 ** Llo[two]
+    io_lo = 1 - np.abs(s64[two] - 2.0 ** Llo[two]) / den
+    io_hi = 1 - np.abs(s64[two] - 2.0 ** Lup[two]) / den
+    assert np.array_equal(iota[two, 0].astype(np.float64), io_lo)
+    assert np.array_equal(iota[two, 1].astype(np.float64), io_hi)
+    assert np.all(iota[two, 0] + iota[two, 1] == 1)
+    assert np.all(iota[~two, 0] == 1)
+    # eps branch (second case of Eq. 4): within 1 ulp of the fp64 value
+    small = rng.uniform(0, 1, 100_000).astype(np.float32)
+    lv, io = levels_for(small, n)
+    assert np.all(lv == 0x20)
+    ref = 0.25 + 0.75 * small.astype(np.float64)
+    assert np.all(np.abs(io[:, 0] - ref) <= np.spacing(np.float32(1.0)))
+
+
+def test_layer_continuity():
+    """approaching 2^k from either side gives iota -> 1 on layer k."""
+    n = 8
+    for k in range(1, n - 1):
+        for d in (-1e-4, 1e-4):
+            lv, io = levels_for([2.0 ** k * (1 + d)], n)
+            layers = decode(int(lv[0]))
+            w = dict(zip(layers, io[0]))
+            assert abs(w.get(k, 0.0) - 1.0) < 1e-3
+    # s = 1 boundary (Q4): both branches give 1
+    lv, io = levels_for([np.nextafter(np.float32(1), np.float32(0)), 1.0], n)
+    assert abs(io[0, 0] - 1.0) < 1e-6 and io[1, 0] == 1.0
+
+
+def test_sw_doubling_shifts_levels_by_one():
+    """P3: doubling s_w shifts the layers by exactly +1 with bit-identical iota, s in [1, 2^(n-2))."""
+    n = 8
+    rng = np.random.default_rng(3)
+    s = (2.0 ** rng.uniform(0, n - 2, 20000)).astype(np.float32)
+    l1, i1 = levels_for(s, n)
+    l2, i2 = levels_for(s * np.float32(2), n)
+    l1, l2 = l1.astype(np.int32), l2.astype(np.int32)
+    assert np.array_equal(l2 & 0x0F, (l1 & 0x0F) + 1)
+    assert np.array_equal(l2 & 0xF0, l1 & 0xF0)
+    assert np.array_equal(i1, i2)
+
+
+# ------------------------------------------------------------------ footprint (P4)
+
+def single_point_layer0(u, v, W=32, H=32, alpha=1.0, s=1.0):
+    cam = unit_cam(W, H, f=16.0)
+    pos, sw, a, d = point_scene(cam, [[u, v, 2.0]], [s], alpha=[alpha])
+    r = oracle.forward(cam, 4, pos, sw, a, d)
+    lay = oracle.split_pyramid(r["pyramid"], 1, W, H, 4)
+    cnt = oracle.split_pixels(r["counts"], W, H, 4)
+    return lay, cnt
+
+
+def test_footprint_spec_examples():
+    for ex in GOLD["footprint"]:
+        lay, cnt = single_point_layer0(*ex["xy"])
+        for key, beta in ex["beta"].items():
+            x, y = map(int, key.split(","))
+            assert cnt[0][y, x] == 1, ex["cite"]                       # zero weight kept (Q9)
+            assert lay[0][1, y, x] == beta, ex["cite"]                 # A = gamma = beta (alpha = iota = 1)
+        assert cnt[0].sum() == 4 and all(c.sum() == 0 for c in cnt[1:])
+
+
+def test_weight_partition():
+    """SPEC.md:236 / 204-206: for in-range sizes the fragments' gamma sum to alpha (1e-6),
+    i.e. sum beta = 1 per layer and iota_lo + iota_hi = 1."""
+    rng = np.random.default_rng(5)
+    W = H = 96
+    cam = unit_cam(W, H, f=48.0)
+    n_layers = 5
+    for _ in range(60):
+        s = 2.0 ** rng.uniform(0, n_layers - 1)
+        u, v = rng.uniform(20, 70, 2)
+        a = rng.uniform(0.1, 1.0)
+        pos, sw, al, d = point_scene(cam, [[u, v, rng.uniform(1, 3)]], [s], alpha=[a])
+        r = oracle.forward(cam, n_layers, pos, sw, al, d)
+        layers = oracle.split_pyramid(r["pyramid"], 1, W, H, n_layers)
+        tot = sum(L[1].sum() for L in layers)                            # A channel = sum gamma
+        assert abs(tot - float(al[0])) < 1e-6
+
+
+# ------------------------------------------------------------------ blending (P7)
+
+def test_blend_spec_examples():
+    for ex in GOLD["blend"]:
+        cam = unit_cam(16, 16, f=8.0)
+        g = ex["gammas"]
+        pts = [[5.0, 5.0, 1.0 + j] for j in range(len(g))]           # pixel centre, layer 0, beta = 1
+        pos, sw, a, d = point_scene(cam, pts, [1.0] * len(g), alpha=g, desc=ex["features"])
+        r = oracle.forward(cam, 3, pos, sw, a, d)
+        lay = oracle.split_pyramid(r["pyramid"], 1, 16, 16, 3)
+        assert lay[0][0, 5, 5] == float(np.float32(ex["C"])) or abs(lay[0][0, 5, 5] - ex["C"]) < 1e-15, ex["cite"]
+        assert lay[0][1, 5, 5] == ex["A"], ex["cite"]
+
+
+def test_opaque_front_occludes_and_cap():
+    """North star: an opaque front point fully occludes; PAPER.md:217 cap of 16: a 40-deep
+    stack keeps exactly the 16 nearest, ordered by depth then index (Q12)."""
+    cam = unit_cam(16, 16, f=8.0)
+    rng = np.random.default_rng(2)
+    zs = rng.permutation(1.0 + np.arange(40) / 32.0)                # dyadic: s == 1 exactly
+    pts = [[7.0, 7.0, z] for z in zs]
+    desc = rng.normal(size=40)
+    pos, sw, a, d = point_scene(cam, pts, [1.0] * 40, alpha=[0.3] * 40, desc=desc)
+    r = oracle.forward(cam, 3, pos, sw, a, d)
+    kept = oracle.split_pixels(r["kept"].reshape(-1), 16, 16, 3, 16)[0][7, 7]
+    cnt = oracle.split_pixels(r["counts"], 16, 16, 3)[0][7, 7]
+    assert cnt == 40
+    assert list(kept) == list(np.argsort(zs)[:16])
+    # analytic blend of the 16 nearest (Eqs. 5-6 closed form for constant gamma)
+    g = float(np.float32(0.3))                                       # alpha as stored (fp32)
+    order = np.argsort(zs)[:16]
+    C = sum((1 - g) ** m * g * float(d[i, 0]) for m, i in enumerate(order))
+    lay = oracle.split_pyramid(r["pyramid"], 1, 16, 16, 3)
+    assert abs(lay[0][0, 7, 7] - C) < 1e-6
+    assert abs(lay[0][1, 7, 7] - (1 - (1 - g) ** 16)) < 1e-12
+    # make the nearest one opaque: it alone decides the pixel
+    a2 = a.copy()
+    a2[order[0]] = 1.0
+    r2 = oracle.forward(cam, 3, pos, sw, a2, d)
+    lay2 = oracle.split_pyramid(r2["pyramid"], 1, 16, 16, 3)
+    assert lay2[0][0, 7, 7] == float(d[order[0], 0]) and lay2[0][1, 7, 7] == 1.0
+
+
+def test_equal_depth_ties_break_on_index():
+    cam = unit_cam(16, 16, f=8.0)
+    pts = [[4.0, 4.0, 2.0]] * 20
+    pos, sw, a, d = point_scene(cam, pts, [1.0] * 20, alpha=[0.5] * 20, desc=np.arange(20.0))
+    r = oracle.forward(cam, 3, pos, sw, a, d)
+    kept = oracle.split_pixels(r["kept"].reshape(-1), 16, 16, 3, 16)[0][4, 4]
+    assert list(kept) == list(range(16))
+
+
+def test_blend_bounds():
+    """descriptors in [0,1] -> every channel in [0,1]."""
+    sc = scenes.tiny_scene(4, n=300)
+    d = np.random.default_rng(0).uniform(0, 1, sc.desc.shape).astype(np.float32)
+    r = oracle.forward(sc.cams[0], sc.n_layers, sc.pos, sc.sw, sc.alpha, d)
+    assert r["pyramid"].min() >= 0 and r["pyramid"].max() <= 1 + 1e-12
+
+
+def test_permutation_invariance():
+    """P7: permuting point indices (no depth ties) leaves the pyramid bit-identical."""
+    sc = scenes.c1()
+    cam = sc.cams[0]
+    r1 = oracle.forward(cam, sc.n_layers, sc.pos, sc.sw, sc.alpha, sc.desc)
+    perm = np.random.default_rng(9).permutation(sc.n)
+    r2 = oracle.forward(cam, sc.n_layers, sc.pos[perm], sc.sw[perm], sc.alpha[perm], sc.desc[perm])
+    assert np.array_equal(r1["pyramid"], r2["pyramid"])
+    assert np.array_equal(r1["counts"], r2["counts"])
+    inv = np.argsort(perm)
+    k2 = np.where(r2["kept"] >= 0, perm[np.maximum(r2["kept"], 0)], -1)
+    assert np.array_equal(r1["kept"], k2)
+    del inv
+
+
+# ------------------------------------------------------------------ brute force (P5)
+
+def _compare_o0_o1(sc):
+    cam = sc.cams[0]
+    r = oracle.forward(cam, sc.n_layers, sc.pos, sc.sw, sc.alpha, sc.desc)
+    L, Cn, K = brute.render(cam, sc.n_layers, sc.pos, sc.sw, sc.alpha, sc.desc)
+    pyr = oracle.split_pyramid(r["pyramid"], sc.F, cam.width, cam.height, sc.n_layers)
+    cn = oracle.split_pixels(r["counts"], cam.width, cam.height, sc.n_layers)
+    kp = oracle.split_pixels(r["kept"].reshape(-1), cam.width, cam.height, sc.n_layers, 16)
+    for l in range(sc.n_layers):
+        assert np.array_equal(cn[l], Cn[l]), (sc.name, l)
+        assert np.array_equal(kp[l], K[l]), (sc.name, l)
+        assert np.abs(pyr[l] - L[l]).max() <= 1e-12, (sc.name, l)
+    assert r["stats"]["n_frag"] == sum(c.sum() for c in Cn)
+
+
+def test_o1_matches_brute_force_c1():
+    _compare_o0_o1(scenes.c1())
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_o1_matches_brute_force_random(seed):
+    _compare_o0_o1(scenes.tiny_scene(seed))
+
+
+def test_o1_matches_brute_force_adversarial():
+    sc = scenes.adversarial_scene()
+    _compare_o0_o1(sc)
+    r = oracle.forward(sc.cams[0], sc.n_layers, sc.pos, sc.sw, sc.alpha, sc.desc)
+    assert r["stats"]["n_culled"] >= 7 and r["stats"]["max_list"] >= 40
+
+
+def test_2k_metamorphic_relation():
+    """P5: render with (2fx, 2fy, 2cx, 2cy, 2f, 2W, 2H, n+1 layers): layer l+1 equals layer l
+    of the original bit for bit for every l >= 1 (power-of-two scaling is exact)."""
+    sc = scenes.c1()
+    cam = sc.cams[0]
+    cam2 = scenes.Camera(fx=2 * cam.fx, fy=2 * cam.fy, cx=2 * cam.cx, cy=2 * cam.cy, f=2 * cam.f, R=cam.R,
+                         t=cam.t, width=2 * cam.width, height=2 * cam.height, near=cam.near)
+    r1 = oracle.forward(cam, sc.n_layers, sc.pos, sc.sw, sc.alpha, sc.desc)
+    r2 = oracle.forward(cam2, sc.n_layers + 1, sc.pos, sc.sw, sc.alpha, sc.desc)
+    W, H, n, F = cam.width, cam.height, sc.n_layers, sc.F
+    p1 = oracle.split_pyramid(r1["pyramid"], F, W, H, n)
+    p2 = oracle.split_pyramid(r2["pyramid"], F, 2 * W, 2 * H, n + 1)
+    c1 = oracle.split_pixels(r1["counts"], W, H, n)
+    c2 = oracle.split_pixels(r2["counts"], 2 * W, 2 * H, n + 1)
+    k1 = oracle.split_pixels(r1["kept"].reshape(-1), W, H, n, 16)
+    k2 = oracle.split_pixels(r2["kept"].reshape(-1), 2 * W, 2 * H, n + 1, 16)
+    for l in range(1, n):
+        assert np.array_equal(c1[l], c2[l + 1])
+        assert np.array_equal(k1[l], k2[l + 1])
+        assert np.array_equal(p1[l], p2[l + 1])
+
+
+# ------------------------------------------------------------------ backward (P8)
+
+def _loss_f64(sc, G, pos, sw, alpha, desc):
+    r = oracle.forward(sc.cams[0], sc.n_layers, pos, sw, alpha, desc, real="double")
+    return float(np.dot(r["pyramid"], G.astype(np.float64))), r
+
+
+def test_backward_zero_and_single_point():
+    """zero upstream gradient -> zero; one fragment: dC/dtau = gamma."""
+    sc = scenes.c1()
+    cam = sc.cams[0]
+    P = oracle.num_pixels(cam.width, cam.height, sc.n_layers)
+    g, _ = oracle.backward(cam, sc.n_layers, sc.pos, sc.sw, sc.alpha, sc.desc,
+                           np.zeros(P * (sc.F + 1), np.float32))
+    assert not g.any()
+    cam1 = unit_cam(16, 16, f=8.0)
+    pos, sw, a, d = point_scene(cam1, [[5.25, 6.5, 2.0]], [1.0], alpha=[0.8], F=2)
+    P1 = oracle.num_pixels(16, 16, 3)
+    G = np.zeros(P1 * 3, np.float32)
+    G[0 * 256 + 6 * 16 + 5] = 1.0                                   # d/dC_0 at pixel (5,6)
+    g, _ = oracle.backward(cam1, 3, pos, sw, a, d, G)
+    gamma = 0.75 * 0.5 * np.float32(0.8)                            # beta = 0.75 * 0.5, iota = 1
+    assert abs(g[0, 5] - gamma) < 1e-7 and g[0, 6] == 0.0
+
+
+def _fd_check(sc, seed, n_coords=60, h_rel=2.0 ** -12, tol=2e-5):
+    cam = sc.cams[0]
+    P = oracle.num_pixels(cam.width, cam.height, sc.n_layers)
+    G = scenes.grad_pyramid(P * (sc.F + 1), seed=seed)
+    g, mag = oracle.backward(cam, sc.n_layers, sc.pos, sc.sw, sc.alpha, sc.desc, G, real="double")
+    params = [sc.pos.copy(), sc.sw.copy(), sc.alpha.copy(), sc.desc.copy()]
+    _, base = _loss_f64(sc, G, *params)
+    _, lev0, _ = oracle.project(cam, sc.n_layers, sc.pos, sc.sw, real="double")
+    rng = np.random.default_rng(seed)
+    checked = 0
+    scale = np.abs(g).max()
+    for _ in range(n_coords):
+        i = int(rng.integers(sc.n))
+        which = int(rng.integers(4 + sc.F))          # 0-2 pos, 3 sw, 4 alpha, 5.. desc
+        if lev0[i] < 0:
+            continue
+        if which < 3:
+            arr, idx, col = 0, (i, which), which
+        elif which == 3:
+            arr, idx, col = 1, (i,), 3
+        elif which == 4:
+            arr, idx, col = 2, (i,), 4
+        else:
+            arr, idx, col = 3, (i, which - 5), which
+        x0 = float(params[arr][idx])
+        h = max(abs(x0), 1e-2) * h_rel
+        vals = []
+        ok = True
+        for sgn in (+1, -1):
+            p = [q.copy() for q in params]
+            p[arr][idx] = np.float32(x0 + sgn * h)
+            L, r = _loss_f64(sc, G, *p)
+            _, lev, _ = oracle.project(cam, sc.n_layers, p[0], p[1], real="double")
+            if (not np.array_equal(r["counts"], base["counts"]) or not np.array_equal(r["kept"], base["kept"])
+                    or not np.array_equal(lev, lev0)):
+                ok = False                            # structural guard: lists/levels changed
+                break
+            vals.append((L, float(p[arr][idx])))
+        if not ok:
+            continue
+        (Lp, xp), (Lm, xm) = vals
+        fd = (Lp - Lm) / (xp - xm)
+        assert abs(fd - g[i, col]) <= tol * scale + 1e-3 * abs(g[i, col]), (i, col, fd, g[i, col])
+        checked += 1
+    assert checked >= n_coords // 3
+    return checked
+
+
+def test_backward_finite_differences_c1():
+    sc = scenes.c1()
+    # keep it quick: a 300-point subset
+    sub = np.random.default_rng(0).choice(sc.n, 300, replace=False)
+    sc.pos, sc.sw, sc.alpha, sc.desc = sc.pos[sub], sc.sw[sub], sc.alpha[sub], sc.desc[sub]
+    _fd_check(sc, seed=11)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_backward_finite_differences_random(seed):
+    _fd_check(scenes.tiny_scene(seed, n=120), seed=seed + 20, n_coords=40)
+
+
+def test_backward_directional_derivative():
+    """<dL/dtheta, v> equals the FD directional derivative (all parameters at once)."""
+    sc = scenes.tiny_scene(7, n=80)
+    cam = sc.cams[0]
+    P = oracle.num_pixels(cam.width, cam.height, sc.n_layers)
+    G = scenes.grad_pyramid(P * (sc.F + 1), seed=3)
+    g, _ = oracle.backward(cam, sc.n_layers, sc.pos, sc.sw, sc.alpha, sc.desc, G, real="double")
+    rng = np.random.default_rng(1)
+    v = [rng.normal(size=a.shape) for a in (sc.pos, sc.sw, sc.alpha, sc.desc)]
+    h = 1e-4
+    Ls = []
+    for sgn in (+1, -1):
+        p = [(a.astype(np.float64) + sgn * h * d).astype(np.float32) for a, d in
+             zip((sc.pos, sc.sw, sc.alpha, sc.desc), v)]
+        Ls.append(_loss_f64(sc, G, *p)[0])
+    # directional derivative from the actual (fp32-rounded) step
+    dirv = np.concatenate([g[:, :3].ravel(), g[:, 3], g[:, 4], g[:, 5:].ravel()])
+    p_plus = [(a.astype(np.float64) + h * d).astype(np.float32).astype(np.float64) for a, d in
+              zip((sc.pos, sc.sw, sc.alpha, sc.desc), v)]
+    p_minus = [(a.astype(np.float64) - h * d).astype(np.float32).astype(np.float64) for a, d in
+               zip((sc.pos, sc.sw, sc.alpha, sc.desc), v)]
+    step = np.concatenate([(pp - pm).ravel() for pp, pm in zip(p_plus, p_minus)])
+    fd = Ls[0] - Ls[1]
+    an = float(np.dot(dirv, step))
+    assert abs(fd - an) <= 1e-3 * np.abs(dirv * step).sum() + 1e-9, (fd, an)
+
+
+def test_multi_view_gradients_sum():
+    """Q21: gradients of several views accumulate (SUM) into one buffer."""
+    sc = scenes.make_config("C4", n=3000, n_views=3)
+    cams = [scenes.look_at(-c.R.T.astype(np.float64) @ c.t.astype(np.float64), [0, 0, 0], 64, 48, 40.0)
+            for c in sc.cams]
+    P = oracle.num_pixels(64, 48, 4)
+    acc = None
+    parts = []
+    for v, cam in enumerate(cams):
+        G = scenes.grad_pyramid(P * 5, seed=v)
+        g, _ = oracle.backward(cam, 4, sc.pos, sc.sw, sc.alpha, sc.desc, G)
+        parts.append(g)
+        acc, _ = oracle.backward(cam, 4, sc.pos, sc.sw, sc.alpha, sc.desc, G, grad=acc)
+    assert np.allclose(acc, sum(parts), rtol=0, atol=1e-12)
