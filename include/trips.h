@@ -1,0 +1,182 @@
+/*
+ * trips.h -- C ABI of the B200-native TRIPS trilinear point-splatting rasterizer.
+ *
+ * The operation is the render function Phi of arXiv 2401.06003, Eq. (1)
+ * restricted to the rasterizer (no environment map, no decoder network):
+ *   camera intrinsics C and pose (R, t), point positions x, world sizes s_w,
+ *   descriptors tau, opacities alpha  ->  an n-layer feature pyramid,
+ * computed in the paper's three stages (Sec. 3.6):
+ *   trips_project        "collecting": project every point, its screen size s = f s_w / z
+ *                        (Eq. 2) and its two pyramid layers
+ *                        (Eq. 4), count the work per pyramid tile;
+ *   trips_splat_forward  "splatting" + "accumulation": bin points into per-tile lists,
+ *                        build per-pixel fragment lists, keep the 16 nearest by
+ *                        (depth, point index) (Sec. 3.2) and
+ *                        alpha-blend them front to back (Eqs. 5-6);
+ *                        the sorted lists are stored for the backward;
+ *   trips_splat_backward gradients w.r.t. positions, world sizes, opacities and
+ *                        descriptors (chain rule of Eqs. 2-6).
+ * Readings of the paper where it is silent are listed in DESIGN.md ("Readings", Q1-Q24).
+ *
+ * CONVENTIONS
+ *  - All array pointers are CUDA DEVICE pointers owned by the caller, except `trips_camera*`,
+ *    `trips_config*`, `trips_stats*` and output scalars, which are host pointers.
+ *  - The library never allocates device memory.  The caller allocates one workspace of
+ *    trips_workspace_bytes() bytes (256-byte aligned, contents need not be initialised) per
+ *    plan; a workspace belongs to one plan.
+ *  - All work is enqueued asynchronously on `stream` (a cudaStream_t, passed as void*; NULL =
+ *    legacy default stream).  Nothing synchronises except trips_read_stats,
+ *    trips_debug_export and trips_read_stage_ms.  Kernel faults surface at the caller's next
+ *    synchronisation.
+ *  - On error a negative trips_status is returned and NOTHING is enqueued.
+ *  - Points that are behind the near plane, non-finite, or have negative size are CULLED
+ *    (counted in the stats), not errors.  alpha outside [0,1] is caller error: results are
+ *    defined arithmetically but meaningless.
+ *  - A plan is not thread-safe; distinct plans/workspaces are independent.
+ */
+#ifndef TRIPS_H_
+#define TRIPS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Pinhole camera (Sec. 3.1).  Pixel (i, j) of layer 0 has its centre at
+ * (i, j); layer l is addressed with x_l = x * 2^-l (reading Q7).  OpenCV axes: x right,
+ * y down, z forward; world -> view p = R x + t (reading Q24). */
+typedef struct {
+    float fx, fy, cx, cy;      /* pixels */
+    float f;                   /* focal length of Eq. (2); callers use sqrt(fx*fy) (Q6) */
+    float R[9];                /* row-major world -> view rotation */
+    float t[3];
+    int32_t width, height;     /* layer-0 size; must equal the plan's */
+    float near_plane;          /* points with !(z > near_plane) are culled (Q14); > 0 */
+} trips_camera;
+
+typedef struct {
+    int32_t num_layers;        /* n in [1, 16]  (paper studies 3..8) */
+    int32_t num_features;      /* F in [1, 32]  (paper uses 4..8) */
+} trips_config;
+
+typedef struct trips_plan trips_plan;   /* opaque, host memory, owned by the library */
+
+typedef struct {
+    int64_t n_culled;          /* points culled in the last trips_project */
+    int64_t n_visible;
+    int64_t n_pairs;           /* (point, pyramid tile) work items */
+    int64_t n_frag;            /* fragments = sum of per-pixel list lengths */
+    int64_t n_kept;            /* sum over pixels of min(16, list length) */
+    int64_t n_trunc_pixels;    /* pixels whose list was longer than 16 */
+    int64_t max_list;          /* longest per-pixel list */
+} trips_stats;
+
+typedef enum {
+    TRIPS_OK = 0,
+    TRIPS_ERR_ARG = -1,        /* null required pointer, n < 0, bad config/camera */
+    TRIPS_ERR_ALIGN = -2,      /* a device pointer violates the alignment stated below */
+    TRIPS_ERR_CAPACITY = -3,   /* n > max_points of the plan */
+    TRIPS_ERR_STATE = -4,      /* call order violated (see each call) or different workspace */
+    TRIPS_ERR_CUDA = -5        /* a launch failed; see trips_status_string */
+} trips_status;
+
+/* Flags of trips_splat_forward. */
+#define TRIPS_FWD_SAVE_FOR_BACKWARD 1u
+
+/* What trips_debug_export copies (into a caller DEVICE buffer). */
+typedef enum {
+    TRIPS_EXPORT_COUNTS = 1,   /* uint32[P]: per-pixel list length, pyramid pixel order     */
+    TRIPS_EXPORT_KEPT = 2      /* int32[P*16]: kept point indices in blend order, -1 padded */
+} trips_export;
+
+/* ---- plan ------------------------------------------------------------------------- */
+
+/* Creates a plan for images of width x height and up to max_points points.
+ * Errors: TRIPS_ERR_ARG (null, bad config, width/height < 1 or > 32768, max_points < 0 or
+ * >= 2^28). */
+int trips_plan_create(const trips_config* cfg, int32_t width, int32_t height, int64_t max_points,
+                      trips_plan** out);
+void trips_plan_destroy(trips_plan* plan);
+
+/* Workspace size in bytes for this plan (caller allocates, 256-B aligned). */
+size_t trips_workspace_bytes(const trips_plan* plan);
+
+/* P = number of pyramid pixels = sum_l ceil(H/2^l) * ceil(W/2^l) (reading Q8). */
+int64_t trips_num_pixels(const trips_plan* plan);
+
+/* Pyramid floats = (F+1) * P.  Layout: layer-major; layer l is planar [(F+1), H_l, W_l];
+ * channel F is the accumulated opacity A = sum_m T_m gamma_m (reading Q16). */
+int64_t trips_pyramid_floats(const trips_plan* plan);
+
+/* Layer l geometry: *h = H_l, *w = W_l, *offset_floats = float offset of layer l in the
+ * pyramid.  Any output pointer may be NULL.  Errors: TRIPS_ERR_ARG (l out of range). */
+int trips_layer_dims(const trips_plan* plan, int32_t l, int32_t* h, int32_t* w,
+                     int64_t* offset_floats);
+
+/* Row stride G (floats) of the packed gradient buffer: G = 8 + 4*ceil(F/4).  Row i holds
+ * (dL/dx, dL/dy, dL/dz, dL/ds_w, dL/dalpha, dL/dtau[0..F-1], zero padding). */
+int32_t trips_grad_stride(const trips_plan* plan);
+
+/* ---- the three stages -------------------------------------------------------------- */
+
+/* Stage 1, "collecting".  Projects the n points (Eq. 2), selects their
+ * layers (Eq. 4) and counts the (point, tile) work per pyramid tile.  Stores per-point
+ * screen records in the workspace.  Starts a new frame on this plan (any saved forward
+ * state is invalidated).
+ *   pos        float[n][3] world positions, 4-byte aligned
+ *   world_size float[n]    s_w
+ *   opacity    float[n]    alpha
+ *   desc       float[n][F] descriptors tau, row-major, 4-byte aligned
+ *   level_out  int8[n]  nullable: -1 culled, else bits 0-3 lowest layer, 0x10 two layers,
+ *                       0x20 eps branch (s < 1), 0x40 clamped (s >= 2^(n-1))
+ *   proj_out   float[n][4] nullable: (x, y, z, s), NaN rows for culled points
+ * Errors: TRIPS_ERR_ARG, TRIPS_ERR_CAPACITY (n > max_points), TRIPS_ERR_ALIGN (ws not 256-B
+ * aligned), TRIPS_ERR_CUDA. */
+int trips_project(trips_plan* plan, void* ws, const trips_camera* cam, int64_t n,
+                  const float* pos, const float* world_size, const float* opacity,
+                  const float* desc, int8_t* level_out, float* proj_out, void* stream);
+
+/* Stages 2-3.  Writes the whole pyramid (trips_pyramid_floats floats,
+ * 16-B aligned).  With TRIPS_FWD_SAVE_FOR_BACKWARD the sorted kept lists stay in the
+ * workspace for trips_splat_backward.  Errors: TRIPS_ERR_STATE (no trips_project since
+ * the plan was created or since the last forward, or ws differs), TRIPS_ERR_ARG,
+ * TRIPS_ERR_ALIGN, TRIPS_ERR_CUDA. */
+int trips_splat_forward(trips_plan* plan, void* ws, float* pyramid, uint32_t flags, void* stream);
+
+/* Backward of the last saved forward.  grad_pyramid has the pyramid layout (16-B aligned).
+ * Gradients are ACCUMULATED (+=) into grad[n][G] (G = trips_grad_stride, 16-B aligned),
+ * so several views sum into one buffer (reading Q21); the caller zeroes it once per batch.
+ * May be called more than once per forward.  Errors: TRIPS_ERR_STATE (last forward not
+ * saved, or ws differs), TRIPS_ERR_ARG, TRIPS_ERR_ALIGN, TRIPS_ERR_CUDA. */
+int trips_splat_backward(trips_plan* plan, void* ws, const float* grad_pyramid, float* grad,
+                         void* stream);
+
+/* ---- introspection ----------------------------------------------------------------- */
+
+/* Synchronises `stream` and reads the statistics of the last project/forward. */
+int trips_read_stats(const trips_plan* plan, const void* ws, trips_stats* out, void* stream);
+
+/* Synchronises `stream` and copies debug state of the last forward into the device buffer
+ * dst (sizes in trips_export).  Errors: TRIPS_ERR_STATE (no forward), TRIPS_ERR_ARG. */
+int trips_debug_export(const trips_plan* plan, const void* ws, int32_t what, void* dst, void* stream);
+
+/* Per-stage device timing.  When enabled, CUDA events bracket every kernel stage
+ * (0 project, 1 scan, 2 bin, 3 raster, 4 backward); trips_read_stage_ms synchronises
+ * the events and returns the accumulated milliseconds and launch counts since the last
+ * reset.  Returns the number of stages written. */
+int trips_set_profiling(trips_plan* plan, int32_t enable);
+int trips_read_stage_ms(trips_plan* plan, double* ms, int64_t* launches, int32_t max_stages,
+                        int32_t reset);
+
+/* Total kernel launches issued by this library in this process. */
+int64_t trips_launch_count(void);
+
+/* Human-readable text for a status code (includes the last CUDA error for TRIPS_ERR_CUDA). */
+const char* trips_status_string(int status);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TRIPS_H_ */

@@ -1,0 +1,187 @@
+// common.cuh -- shared device definitions of the B200 TRIPS rasterizer.
+//
+// The "exact block" (projection, layer selection, footprint, beta, gamma) uses explicitly
+// rounded intrinsics (__fmul_rn/__fadd_rn/__fdiv_rn/__fsub_rn) so that nvcc can neither
+// contract to FMA nor reorder: levels, pixel indices and counts are then bit-identical to
+// any IEEE evaluation of the same sequence.  Never compile this
+// with --use_fast_math or -ftz=true.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace trips {
+
+constexpr int kTile = 16;                 // pyramid tiles are 16 x 16 pixels
+constexpr int kTilePix = kTile * kTile;   // one CTA thread per tile pixel
+constexpr int kCap = 16;                  // "clamped to a maximum size of 16"
+constexpr int kMaxLayers = 16;
+constexpr float kEps = 0.25f;             // "at least eps = 0.25"
+constexpr uint64_t kKeyMax = ~0ull;
+constexpr float kCulled = -1.0f;          // rec.s marker of a culled point
+
+struct LayerGeom {
+    int32_t W, H;          // ceil(W0 / 2^l), ceil(H0 / 2^l)   (reading Q8)
+    int32_t tiles_x, tiles_y;
+    int32_t tile_base;     // first global tile id of this layer
+    int32_t pad;
+    int64_t pix_off;       // pyramid pixel offset of the layer (pixel order of the export)
+    int64_t float_off;     // pyramid float offset = pix_off * (F + 1)
+};
+
+struct Cam {
+    float fx, fy, cx, cy, f;
+    float R[9], t[3];
+    float near_plane;
+};
+
+// Everything a kernel needs, passed by value (fits the 32 KB kernel-parameter space).
+struct Params {
+    int32_t n, F, FC, RS, G;          // F features, FC = round_up(F,4), RS = 4 + FC, G = 8 + FC
+    int32_t n_layers, T;              // layers, total tiles
+    int32_t pad0;
+    LayerGeom L[kMaxLayers];
+    Cam cam;
+    // inputs (caller)
+    const float* pos; const float* sw; const float* alpha; const float* desc;
+    // workspace
+    float* rec;            // [n][RS]  (x, y, s, alpha, tau[FC])     s < 0 marks culled
+    float* zbuf;           // [n]      view depth z
+    uint32_t* tile_cnt;    // [T]      (point, tile) pairs per tile
+    uint32_t* tile_off;    // [T+1]    exclusive scan of tile_cnt
+    uint32_t* tile_cur;    // [T]      fill cursors
+    uint32_t* tile_kbase;  // [T+1]    kept-list base per tile (scan of min(4096, 4 cnt))
+    uint32_t* bins;        // [8n]     point index per (tile, pair)
+    uint32_t* pix_cnt;     // [T*256]  list length per tile pixel
+    uint32_t* pix_meta;    // [T*256]  (local kept offset << 5) | K
+    uint64_t* kept;        // [kcap]   kept (z, i) keys, per pixel in blend order
+    unsigned long long* stats;  // [8]  n_culled, n_visible, n_pairs, n_frag, n_kept, n_trunc, max_list
+};
+
+enum StatIdx { S_CULLED = 0, S_VISIBLE, S_PAIRS, S_FRAG, S_KEPT, S_TRUNC, S_MAXLIST, S_COUNT };
+
+// --------------------------------------------------------------------------- exact block
+
+// Sec. 3.1.  p = R x + t with pinned order ((R0 X + R1 Y) + R2 Z) + t,
+// x = (fx p_x) / z + cx, y = (fy p_y) / z + cy, s = (f s_w) / z.  Returns false if culled
+// (reading Q14: !(z > near), or x, y, s non-finite, or s < 0).
+__device__ __forceinline__ bool project_exact(const Cam& c, float X, float Y, float Z, float sw,
+                                              float& xs, float& ys, float& z, float& s)
+{
+    float p[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+        float a = __fmul_rn(c.R[3 * r + 0], X);
+        float b = __fmul_rn(c.R[3 * r + 1], Y);
+        float d = __fmul_rn(c.R[3 * r + 2], Z);
+        float acc = __fadd_rn(a, b);
+        acc = __fadd_rn(acc, d);
+        p[r] = __fadd_rn(acc, c.t[r]);
+    }
+    z = p[2];
+    if (!(z > c.near_plane)) return false;
+    xs = __fadd_rn(__fdiv_rn(__fmul_rn(c.fx, p[0]), z), c.cx);
+    ys = __fadd_rn(__fdiv_rn(__fmul_rn(c.fy, p[1]), z), c.cy);
+    s = __fdiv_rn(__fmul_rn(c.f, sw), z);
+    if (!isfinite(xs) || !isfinite(ys) || !isfinite(s) || s < 0.0f) return false;
+    return true;
+}
+
+// Layer selection, readings Q1-Q5.  Returns the number of layers (1/2),
+// the lowest layer, the weights iota[2] and d iota / d s (right derivative at kinks, Q19).
+// Level code: bits 0-3 lowest layer, 0x10 two layers, 0x20 eps branch, 0x40 clamp.
+struct Levels {
+    int n, lo, code;
+    float iota[2];
+    float diota[2];
+};
+
+__device__ __forceinline__ Levels select_levels(float s, int n_layers)
+{
+    Levels L;
+    if (s < 1.0f) {                                  // second case of Eq. (4), reading Q3
+        L.n = 1; L.lo = 0; L.code = 0x20;
+        L.iota[0] = __fadd_rn(kEps, __fmul_rn(1.0f - kEps, s));
+        L.diota[0] = 1.0f - kEps;
+        L.iota[1] = 0.0f; L.diota[1] = 0.0f;
+        return L;
+    }
+    const uint32_t bits = __float_as_uint(s);        // s >= 1 and finite: normal number
+    const int k = (int)(bits >> 23) - 127;           // floor(log2 s), exact
+    if (k >= n_layers - 1) {                         // reading Q5: clamp
+        L.n = 1; L.lo = n_layers - 1; L.code = 0x40 | (n_layers - 1);
+        L.iota[0] = 1.0f; L.diota[0] = 0.0f; L.iota[1] = 0.0f; L.diota[1] = 0.0f;
+        return L;
+    }
+    const float m = __uint_as_float((bits & 0x007FFFFFu) | 0x3F800000u);   // s / 2^k in [1,2)
+    const float inv = __uint_as_float((uint32_t)(127 - k) << 23);         // 2^-k
+    L.lo = k;
+    if (m == 1.0f) {                                 // reading Q2: s == 2^k
+        L.n = 1; L.code = k;
+        L.iota[0] = 1.0f; L.diota[0] = -inv; L.iota[1] = 0.0f; L.diota[1] = 0.0f;
+        return L;
+    }
+    // first case of Eq. (4): 1 - |s - 2^L| / (2^(k+1) - 2^k) = 2 - m (L = k), m - 1 (L = k+1)
+    L.n = 2; L.code = 0x10 | k;
+    L.iota[0] = __fsub_rn(2.0f, m); L.diota[0] = -inv;
+    L.iota[1] = __fsub_rn(m, 1.0f); L.diota[1] = inv;
+    return L;
+}
+
+// 2^-l as an exact float
+__device__ __forceinline__ float pow2_neg(int l) { return __uint_as_float((uint32_t)(127 - l) << 23); }
+
+// Footprint of a point in layer l (Eq. 3, readings Q7, Q9): x_l = x * 2^-l; the layer is
+// skipped unless -1 <= x_l < W_l and -1 <= y_l < H_l; x0 = floor(x_l), fx = x_l - x0.
+struct Foot {
+    int x0, y0;
+    float fx, fy;
+};
+
+__device__ __forceinline__ bool footprint(float xs, float ys, int l, int Wl, int Hl, Foot& f)
+{
+    const float sc = pow2_neg(l);
+    const float xl = __fmul_rn(xs, sc), yl = __fmul_rn(ys, sc);
+    if (!(xl >= -1.0f && xl < (float)Wl && yl >= -1.0f && yl < (float)Hl)) return false;
+    const float fx0 = floorf(xl), fy0 = floorf(yl);
+    f.x0 = (int)fx0; f.y0 = (int)fy0;
+    f.fx = __fsub_rn(xl, fx0); f.fy = __fsub_rn(yl, fy0);
+    return true;
+}
+
+// (point, tile) pairs of a point: for each selected layer the tiles touched by the
+// in-bounds pixels of its 2x2 footprint.  Deterministic in (xs, ys, s) so K1 (count) and
+// K3 (fill) enumerate identical lists.  Returns the count (<= 8); optionally the number
+// of in-bounds footprint pixels (= fragments of the point).
+__device__ __forceinline__ int enumerate_pairs(const Params& P, float xs, float ys, float s,
+                                               int tiles[8], int* n_frag)
+{
+    int np = 0, nf = 0;
+    const Levels lv = select_levels(s, P.n_layers);
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        if (k >= lv.n) break;
+        const int l = lv.lo + k;
+        const LayerGeom& G = P.L[l];
+        Foot f;
+        if (!footprint(xs, ys, l, G.W, G.H, f)) continue;
+        const int xa = max(f.x0, 0), xb = min(f.x0 + 1, G.W - 1);
+        const int ya = max(f.y0, 0), yb = min(f.y0 + 1, G.H - 1);
+        if (xa > xb || ya > yb) continue;
+        nf += (xb - xa + 1) * (yb - ya + 1);
+        const int tx0 = xa >> 4, tx1 = xb >> 4, ty0 = ya >> 4, ty1 = yb >> 4;
+        for (int ty = ty0; ty <= ty1; ++ty)
+            for (int tx = tx0; tx <= tx1; ++tx) tiles[np++] = G.tile_base + ty * G.tiles_x + tx;
+    }
+    if (n_frag) *n_frag = nf;
+    return np;
+}
+
+// u64 compare-exchange: (a, b) <- (min, max)
+__device__ __forceinline__ void cswap(uint64_t& a, uint64_t& b)
+{
+    const uint64_t lo = a < b ? a : b;
+    const uint64_t hi = a < b ? b : a;
+    a = lo; b = hi;
+}
+
+}  // namespace trips

@@ -1,0 +1,380 @@
+// trips_api.cu -- host side of the C ABI declared in include/trips.h.
+//
+// Validation, plan/workspace layout, launch sequencing and optional per-stage CUDA-event
+// timing.  No device allocation, no host synchronisation on the hot path.
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "../../include/trips.h"
+#include "kernels.cuh"
+
+using namespace trips;
+
+namespace {
+
+std::atomic<long long> g_launches{0};
+thread_local char g_msg[256];
+
+constexpr int kStages = 5;   // 0 project, 1 scan, 2 bin, 3 raster, 4 backward
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct EventPair {
+    cudaEvent_t a, b;
+};
+
+}  // namespace
+
+struct trips_plan {
+    int32_t n_layers, F, FC, RS, G, W, H, T;
+    int64_t max_points, P, pyr_floats;
+    LayerGeom L[kMaxLayers];
+    uint64_t kcap;
+    // workspace layout (byte offsets)
+    size_t off_rec, off_z, off_tcnt, off_toff, off_tcur, off_tkb, off_bins, off_pcnt, off_pmeta, off_kept,
+        off_stats, ws_bytes;
+    // state
+    const void* ws_bound = nullptr;
+    int stage = 0;          // 0 none, 1 projected, 2 forward (saved), 3 forward (not saved)
+    int64_t n = 0;
+    Cam cam;
+    // profiling
+    bool prof = false;
+    std::vector<EventPair> pending[kStages];
+    std::vector<cudaEvent_t> pool;
+    double ms[kStages] = {0, 0, 0, 0, 0};
+    long long launches[kStages] = {0, 0, 0, 0, 0};
+};
+
+namespace {
+
+cudaEvent_t get_event(trips_plan* p)
+{
+    if (!p->pool.empty()) {
+        cudaEvent_t e = p->pool.back();
+        p->pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+struct StageScope {
+    trips_plan* p;
+    int s;
+    cudaStream_t st;
+    EventPair ev{};
+    StageScope(trips_plan* p_, int s_, cudaStream_t st_) : p(p_), s(s_), st(st_)
+    {
+        if (p->prof) {
+            ev.a = get_event(p);
+            ev.b = get_event(p);
+            cudaEventRecord(ev.a, st);
+        }
+        p->launches[s]++;
+        g_launches++;
+    }
+    ~StageScope()
+    {
+        if (p->prof) {
+            cudaEventRecord(ev.b, st);
+            p->pending[s].push_back(ev);
+        }
+    }
+};
+
+int cuda_status(cudaError_t e)
+{
+    if (e == cudaSuccess) return TRIPS_OK;
+    snprintf(g_msg, sizeof(g_msg), "TRIPS_ERR_CUDA: %s", cudaGetErrorString(e));
+    return TRIPS_ERR_CUDA;
+}
+
+int check_launch() { return cuda_status(cudaGetLastError()); }
+
+Params make_params(const trips_plan* p, void* ws)
+{
+    Params P;
+    memset(&P, 0, sizeof(P));
+    P.n = (int32_t)p->n;
+    P.F = p->F; P.FC = p->FC; P.RS = p->RS; P.G = p->G;
+    P.n_layers = p->n_layers; P.T = p->T;
+    for (int l = 0; l < kMaxLayers; ++l) P.L[l] = p->L[l];
+    P.cam = p->cam;
+    char* b = static_cast<char*>(ws);
+    P.rec = reinterpret_cast<float*>(b + p->off_rec);
+    P.zbuf = reinterpret_cast<float*>(b + p->off_z);
+    P.tile_cnt = reinterpret_cast<uint32_t*>(b + p->off_tcnt);
+    P.tile_off = reinterpret_cast<uint32_t*>(b + p->off_toff);
+    P.tile_cur = reinterpret_cast<uint32_t*>(b + p->off_tcur);
+    P.tile_kbase = reinterpret_cast<uint32_t*>(b + p->off_tkb);
+    P.bins = reinterpret_cast<uint32_t*>(b + p->off_bins);
+    P.pix_cnt = reinterpret_cast<uint32_t*>(b + p->off_pcnt);
+    P.pix_meta = reinterpret_cast<uint32_t*>(b + p->off_pmeta);
+    P.kept = reinterpret_cast<uint64_t*>(b + p->off_kept);
+    P.stats = reinterpret_cast<unsigned long long*>(b + p->off_stats);
+    return P;
+}
+
+bool aligned(const void* ptr, size_t a) { return (reinterpret_cast<uintptr_t>(ptr) & (a - 1)) == 0; }
+
+#define TRIPS_FC_SWITCH(FC, CALL)                \
+    switch (FC) {                                \
+    case 4: { constexpr int kFC = 4; CALL; } break;   \
+    case 8: { constexpr int kFC = 8; CALL; } break;   \
+    case 12: { constexpr int kFC = 12; CALL; } break; \
+    case 16: { constexpr int kFC = 16; CALL; } break; \
+    case 20: { constexpr int kFC = 20; CALL; } break; \
+    case 24: { constexpr int kFC = 24; CALL; } break; \
+    case 28: { constexpr int kFC = 28; CALL; } break; \
+    case 32: { constexpr int kFC = 32; CALL; } break; \
+    default: return TRIPS_ERR_ARG;               \
+    }
+
+}  // namespace
+
+extern "C" {
+
+int trips_plan_create(const trips_config* cfg, int32_t width, int32_t height, int64_t max_points,
+                      trips_plan** out)
+{
+    if (!cfg || !out) return TRIPS_ERR_ARG;
+    *out = nullptr;
+    const int n = cfg->num_layers, F = cfg->num_features;
+    if (n < 1 || n > kMaxLayers || F < 1 || F > 32) return TRIPS_ERR_ARG;
+    if (width < 1 || height < 1 || width > 32768 || height > 32768) return TRIPS_ERR_ARG;
+    if (max_points < 0 || max_points >= (int64_t(1) << 28)) return TRIPS_ERR_ARG;
+    trips_plan* p = new trips_plan();
+    p->n_layers = n; p->F = F; p->FC = (F + 3) & ~3; p->RS = 4 + p->FC; p->G = 8 + p->FC;
+    p->W = width; p->H = height; p->max_points = max_points;
+    memset(p->L, 0, sizeof(p->L));
+    int64_t pix = 0;
+    int32_t tiles = 0;
+    for (int l = 0; l < n; ++l) {
+        LayerGeom& g = p->L[l];
+        g.W = (width + (1 << l) - 1) >> l;
+        g.H = (height + (1 << l) - 1) >> l;
+        g.tiles_x = (g.W + kTile - 1) / kTile;
+        g.tiles_y = (g.H + kTile - 1) / kTile;
+        g.tile_base = tiles;
+        g.pix_off = pix;
+        g.float_off = pix * (F + 1);
+        pix += (int64_t)g.W * g.H;
+        tiles += g.tiles_x * g.tiles_y;
+    }
+    p->P = pix;
+    p->T = tiles;
+    p->pyr_floats = pix * (F + 1);
+    const uint64_t kc1 = (uint64_t)tiles * kTilePix * kCap, kc2 = (uint64_t)max_points * 32;
+    p->kcap = kc1 < kc2 ? kc1 : kc2;
+    if (p->kcap >= (uint64_t(1) << 32)) { delete p; return TRIPS_ERR_ARG; }
+    const size_t N = (size_t)(max_points > 0 ? max_points : 1);
+    size_t o = 0;
+    p->off_rec = o;   o = align256(o + N * p->RS * sizeof(float));
+    p->off_z = o;     o = align256(o + N * sizeof(float));
+    p->off_tcnt = o;  o = align256(o + (size_t)tiles * 4);
+    p->off_toff = o;  o = align256(o + ((size_t)tiles + 1) * 4);
+    p->off_tcur = o;  o = align256(o + (size_t)tiles * 4);
+    p->off_tkb = o;   o = align256(o + ((size_t)tiles + 1) * 4);
+    p->off_bins = o;  o = align256(o + 8 * N * 4);
+    p->off_pcnt = o;  o = align256(o + (size_t)tiles * kTilePix * 4);
+    p->off_pmeta = o; o = align256(o + (size_t)tiles * kTilePix * 4);
+    p->off_kept = o;  o = align256(o + (p->kcap ? p->kcap : 1) * 8);
+    p->off_stats = o; o = align256(o + S_COUNT * 8);
+    p->ws_bytes = o;
+    *out = p;
+    return TRIPS_OK;
+}
+
+void trips_plan_destroy(trips_plan* p)
+{
+    if (!p) return;
+    for (int s = 0; s < kStages; ++s)
+        for (auto& e : p->pending[s]) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
+    for (auto e : p->pool) cudaEventDestroy(e);
+    delete p;
+}
+
+size_t trips_workspace_bytes(const trips_plan* p) { return p ? p->ws_bytes : 0; }
+int64_t trips_num_pixels(const trips_plan* p) { return p ? p->P : -1; }
+int64_t trips_pyramid_floats(const trips_plan* p) { return p ? p->pyr_floats : -1; }
+int32_t trips_grad_stride(const trips_plan* p) { return p ? p->G : -1; }
+
+int trips_layer_dims(const trips_plan* p, int32_t l, int32_t* h, int32_t* w, int64_t* off)
+{
+    if (!p || l < 0 || l >= p->n_layers) return TRIPS_ERR_ARG;
+    if (h) *h = p->L[l].H;
+    if (w) *w = p->L[l].W;
+    if (off) *off = p->L[l].float_off;
+    return TRIPS_OK;
+}
+
+int trips_project(trips_plan* p, void* ws, const trips_camera* c, int64_t n, const float* pos,
+                  const float* world_size, const float* opacity, const float* desc, int8_t* level_out,
+                  float* proj_out, void* stream)
+{
+    if (!p || !ws || !c) return TRIPS_ERR_ARG;
+    if (n < 0) return TRIPS_ERR_ARG;
+    if (n > p->max_points) return TRIPS_ERR_CAPACITY;
+    if (n > 0 && (!pos || !world_size || !opacity || !desc)) return TRIPS_ERR_ARG;
+    if (c->width != p->W || c->height != p->H) return TRIPS_ERR_ARG;
+    if (!(c->fx > 0) || !(c->fy > 0) || !(c->f > 0) || !(c->near_plane > 0)) return TRIPS_ERR_ARG;
+    if (!aligned(ws, 256)) return TRIPS_ERR_ALIGN;
+    if (!aligned(pos, 4) || !aligned(desc, 4) || !aligned(world_size, 4) || !aligned(opacity, 4) ||
+        !aligned(proj_out, 16))
+        return TRIPS_ERR_ALIGN;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    p->ws_bound = ws;
+    p->stage = 0;
+    p->n = n;
+    Cam& cam = p->cam;
+    cam.fx = c->fx; cam.fy = c->fy; cam.cx = c->cx; cam.cy = c->cy; cam.f = c->f;
+    memcpy(cam.R, c->R, sizeof(cam.R));
+    memcpy(cam.t, c->t, sizeof(cam.t));
+    cam.near_plane = c->near_plane;
+    Params P = make_params(p, ws);
+    P.pos = pos; P.sw = world_size; P.alpha = opacity; P.desc = desc;
+    int rc = cuda_status(cudaMemsetAsync(P.tile_cnt, 0, (size_t)p->T * 4, st));
+    if (rc) return rc;
+    rc = cuda_status(cudaMemsetAsync(P.stats, 0, S_COUNT * 8, st));
+    if (rc) return rc;
+    if (n > 0) {
+        StageScope sc(p, 0, st);
+        const int blocks = (int)((n + 255) / 256);
+        TRIPS_FC_SWITCH(p->FC, (k_project<kFC><<<blocks, 256, 0, st>>>(P, level_out, proj_out)));
+        rc = check_launch();
+        if (rc) return rc;
+    }
+    p->stage = 1;
+    return TRIPS_OK;
+}
+
+int trips_splat_forward(trips_plan* p, void* ws, float* pyramid, uint32_t flags, void* stream)
+{
+    if (!p || !ws || !pyramid) return TRIPS_ERR_ARG;
+    if (p->stage != 1 || ws != p->ws_bound) return TRIPS_ERR_STATE;
+    if (!aligned(pyramid, 16)) return TRIPS_ERR_ALIGN;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    Params P = make_params(p, ws);
+    int rc;
+    {
+        StageScope sc(p, 1, st);
+        k_scan<<<1, 1024, 0, st>>>(P);
+        if ((rc = check_launch())) return rc;
+    }
+    if (p->n > 0) {
+        StageScope sc(p, 2, st);
+        k_bin<<<(int)((p->n + 255) / 256), 256, 0, st>>>(P);
+        if ((rc = check_launch())) return rc;
+    }
+    {
+        StageScope sc(p, 3, st);
+        const int save = (flags & TRIPS_FWD_SAVE_FOR_BACKWARD) ? 1 : 0;
+        TRIPS_FC_SWITCH(p->FC, (k_raster<kFC><<<p->T, kTilePix, 0, st>>>(P, pyramid, save)));
+        if ((rc = check_launch())) return rc;
+    }
+    p->stage = (flags & TRIPS_FWD_SAVE_FOR_BACKWARD) ? 2 : 3;
+    return TRIPS_OK;
+}
+
+int trips_splat_backward(trips_plan* p, void* ws, const float* grad_pyramid, float* grad, void* stream)
+{
+    if (!p || !ws || !grad_pyramid || !grad) return TRIPS_ERR_ARG;
+    if (p->stage != 2 || ws != p->ws_bound) return TRIPS_ERR_STATE;
+    if (!aligned(grad_pyramid, 16) || !aligned(grad, 16)) return TRIPS_ERR_ALIGN;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    Params P = make_params(p, ws);
+    int rc;
+    {
+        StageScope sc(p, 4, st);
+        TRIPS_FC_SWITCH(p->FC, (k_backward<kFC><<<p->T, kTilePix, 0, st>>>(P, grad_pyramid, grad)));
+        if ((rc = check_launch())) return rc;
+    }
+    return TRIPS_OK;
+}
+
+int trips_read_stats(const trips_plan* p, const void* ws, trips_stats* out, void* stream)
+{
+    if (!p || !ws || !out) return TRIPS_ERR_ARG;
+    if (p->stage == 0 || ws != p->ws_bound) return TRIPS_ERR_STATE;
+    unsigned long long h[S_COUNT];
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    int rc = cuda_status(cudaMemcpyAsync(h, static_cast<const char*>(ws) + p->off_stats, sizeof(h),
+                                         cudaMemcpyDeviceToHost, st));
+    if (rc) return rc;
+    if ((rc = cuda_status(cudaStreamSynchronize(st)))) return rc;
+    out->n_culled = (int64_t)h[S_CULLED];
+    out->n_visible = (int64_t)h[S_VISIBLE];
+    out->n_pairs = (int64_t)h[S_PAIRS];
+    out->n_frag = (int64_t)h[S_FRAG];
+    out->n_kept = (int64_t)h[S_KEPT];
+    out->n_trunc_pixels = (int64_t)h[S_TRUNC];
+    out->max_list = (int64_t)h[S_MAXLIST];
+    return TRIPS_OK;
+}
+
+int trips_debug_export(const trips_plan* p, const void* ws, int32_t what, void* dst, void* stream)
+{
+    if (!p || !ws || !dst) return TRIPS_ERR_ARG;
+    if (what != TRIPS_EXPORT_COUNTS && what != TRIPS_EXPORT_KEPT) return TRIPS_ERR_ARG;
+    if (ws != p->ws_bound || p->stage < 2) return TRIPS_ERR_STATE;
+    if (what == TRIPS_EXPORT_KEPT && p->stage != 2) return TRIPS_ERR_STATE;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    Params P = make_params(p, const_cast<void*>(ws));
+    g_launches++;
+    k_export<<<p->T, kTilePix, 0, st>>>(P, what, dst);
+    int rc = check_launch();
+    if (rc) return rc;
+    return cuda_status(cudaStreamSynchronize(st));
+}
+
+int trips_set_profiling(trips_plan* p, int32_t enable)
+{
+    if (!p) return TRIPS_ERR_ARG;
+    p->prof = enable != 0;
+    return TRIPS_OK;
+}
+
+int trips_read_stage_ms(trips_plan* p, double* ms, int64_t* launches, int32_t max_stages, int32_t reset)
+{
+    if (!p) return TRIPS_ERR_ARG;
+    for (int s = 0; s < kStages; ++s) {
+        for (auto& e : p->pending[s]) {
+            float t = 0.f;
+            if (cudaEventSynchronize(e.b) == cudaSuccess && cudaEventElapsedTime(&t, e.a, e.b) == cudaSuccess)
+                p->ms[s] += t;
+            p->pool.push_back(e.a);
+            p->pool.push_back(e.b);
+        }
+        p->pending[s].clear();
+    }
+    const int m = max_stages < kStages ? max_stages : kStages;
+    for (int s = 0; s < m; ++s) {
+        if (ms) ms[s] = p->ms[s];
+        if (launches) launches[s] = p->launches[s];
+    }
+    if (reset)
+        for (int s = 0; s < kStages; ++s) { p->ms[s] = 0; p->launches[s] = 0; }
+    return m;
+}
+
+int64_t trips_launch_count(void) { return (int64_t)g_launches.load(); }
+
+const char* trips_status_string(int status)
+{
+    switch (status) {
+    case TRIPS_OK: return "TRIPS_OK";
+    case TRIPS_ERR_ARG: return "TRIPS_ERR_ARG: invalid argument";
+    case TRIPS_ERR_ALIGN: return "TRIPS_ERR_ALIGN: misaligned pointer";
+    case TRIPS_ERR_CAPACITY: return "TRIPS_ERR_CAPACITY: n exceeds the plan's max_points";
+    case TRIPS_ERR_STATE: return "TRIPS_ERR_STATE: call order violated or workspace mismatch";
+    case TRIPS_ERR_CUDA: return g_msg[0] ? g_msg : "TRIPS_ERR_CUDA";
+    default: return "unknown status";
+    }
+}
+
+}  // extern "C"

@@ -1,0 +1,312 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bars (BASELINE.json north_star):
+  bit-exact  projected records (x, y, z, s), level codes, per-pixel counts, kept lists
+  features   |C_gpu - C_oracle| <= 1e-5 * M_C   (M_C = sum_m T_m gamma_m |tau|, per channel)
+  gradients  |g_gpu - g_oracle| <= 1e-3 * M_g   (M_g = the chain with |.| of every factor)
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle
+from synth import scenes
+
+pytestmark = pytest.mark.gpu
+
+FEAT_TOL = 1e-5
+GRAD_TOL = 1e-3
+
+
+@pytest.fixture(scope="module")
+def dev():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2401_06003_b200 import _abi
+    _abi.lib()
+    return torch.device("cuda:0")
+
+
+def T(a, dev):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+
+
+def gpu_run(sc, dev, cam=None, G=None, save=True, export=True):
+    from paper_2401_06003_b200 import Rasterizer
+    cam = cam or sc.cams[0]
+    r = Rasterizer(cam.width, cam.height, sc.n_layers, sc.F, max_points=max(sc.n, 1), device=dev)
+    pos, sw, al, de = (T(a, dev) for a in (sc.pos, sc.sw, sc.alpha, sc.desc))
+    level = torch.empty(sc.n, dtype=torch.int8, device=dev)
+    proj = torch.empty(sc.n, 4, dtype=torch.float32, device=dev)
+    r.project(cam, pos, sw, al, de, level_out=level, proj_out=proj)
+    pyr = r.forward(save=save)
+    out = dict(pyr=pyr.cpu().numpy(), level=level.cpu().numpy(), proj=proj.cpu().numpy(), stats=r.stats(), r=r)
+    if export:
+        out["counts"] = r.export_counts().cpu().numpy().astype(np.uint32)
+        if save:
+            out["kept"] = r.export_kept().cpu().numpy()
+    if G is not None:
+        g = r.backward(T(G, dev))
+        gg = g.cpu().numpy()
+        F = sc.F
+        out["grad"] = np.concatenate([gg[:, :5], gg[:, 5:5 + F]], 1).astype(np.float64)
+        out["grad_pad"] = gg[:, 5 + F:]
+    torch.cuda.synchronize()
+    return out
+
+
+def check_forward(sc, got, cam=None, mask=None):
+    cam = cam or sc.cams[0]
+    ref = oracle.forward(cam, sc.n_layers, sc.pos, sc.sw, sc.alpha, sc.desc, mask=mask)
+    proj, level, _ = oracle.project(cam, sc.n_layers, sc.pos, sc.sw)
+    # bit-exact block
+    assert np.array_equal(got["level"], level), "level codes differ"
+    assert np.array_equal(got["proj"].view(np.uint32), proj.view(np.uint32)), "projected records differ"
+    if mask is None:
+        assert np.array_equal(got["counts"], ref["counts"]), "counts differ"
+        if "kept" in got:
+            assert np.array_equal(got["kept"], ref["kept"]), "kept lists differ"
+        st = got["stats"]
+        for k in ("n_culled", "n_visible", "n_frag", "n_kept", "n_trunc_pixels", "max_list"):
+            assert st[k] == ref["stats"][k], (k, st[k], ref["stats"][k])
+        sel = slice(None)
+        pix = slice(None)
+    else:
+        pix = np.nonzero(mask)[0]
+        assert np.array_equal(got["counts"][pix], ref["counts"][pix]), "counts differ (sampled)"
+        if "kept" in got:
+            assert np.array_equal(got["kept"][pix], ref["kept"][pix]), "kept lists differ (sampled)"
+        F1 = sc.F + 1
+        sel = pixel_float_index(cam, sc.n_layers, F1, pix)
+    err = np.abs(got["pyr"].astype(np.float64)[sel] - ref["pyramid"][sel])
+    bound = FEAT_TOL * ref["mag"][sel] + 1e-30
+    bad = err > bound
+    assert not bad.any(), f"{bad.sum()} features out of tolerance, worst {err.max():.3e}"
+    return ref
+
+
+def pixel_float_index(cam, n_layers, F1, pix):
+    """Float indices of all channels of the given pyramid pixels."""
+    dims = oracle.layer_dims(cam.width, cam.height, n_layers)
+    offs = np.cumsum([0] + [h * w for (h, w) in dims])
+    out = []
+    for l, (h, w) in enumerate(dims):
+        sel = pix[(pix >= offs[l]) & (pix < offs[l + 1])] - offs[l]
+        for c in range(F1):
+            out.append(offs[l] * F1 + c * h * w + sel)
+    return np.concatenate(out)
+
+
+def check_backward(sc, got, G, cam=None, mask=None):
+    cam = cam or sc.cams[0]
+    g, gm = oracle.backward(cam, sc.n_layers, sc.pos, sc.sw, sc.alpha, sc.desc, G, mask=mask)
+    err = np.abs(got["grad"] - g)
+    bad = err > GRAD_TOL * gm + 1e-30
+    assert not bad.any(), f"{bad.sum()} gradient entries out of tolerance; worst rel " \
+                          f"{(err / np.maximum(gm, 1e-30)).max():.3e}"
+    assert not got["grad_pad"].any()
+    rel_l2 = np.linalg.norm(got["grad"] - g) / max(np.linalg.norm(g), 1e-30)
+    assert rel_l2 < 1e-4, rel_l2
+
+
+def grads_for(sc, cam, seed=100, mask=None):
+    P = oracle.num_pixels(cam.width, cam.height, sc.n_layers)
+    G = scenes.grad_pyramid(P * (sc.F + 1), seed=seed)
+    if mask is not None:
+        keep = np.zeros(G.size, bool)
+        keep[pixel_float_index(cam, sc.n_layers, sc.F + 1, np.nonzero(mask)[0])] = True
+        G = np.where(keep, G, 0).astype(np.float32)
+    return G
+
+
+# ------------------------------------------------------------------ small scenes
+
+def test_c1_forward_backward(dev):
+    sc = scenes.c1()
+    G = grads_for(sc, sc.cams[0])
+    got = gpu_run(sc, dev, G=G)
+    check_forward(sc, got)
+    check_backward(sc, got, G)
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_random_tiny_scenes(dev, seed):
+    sc = scenes.tiny_scene(seed)
+    G = grads_for(sc, sc.cams[0], seed=seed)
+    got = gpu_run(sc, dev, G=G)
+    check_forward(sc, got)
+    check_backward(sc, got, G)
+
+
+def test_adversarial_scene(dev):
+    sc = scenes.adversarial_scene()
+    G = grads_for(sc, sc.cams[0], seed=5)
+    got = gpu_run(sc, dev, G=G)
+    check_forward(sc, got)
+    check_backward(sc, got, G)
+    assert got["stats"]["max_list"] >= 40
+
+
+@pytest.mark.parametrize("F", [1, 3, 5, 8, 13])
+def test_feature_counts(dev, F):
+    sc = scenes.tiny_scene(3, n=500, F=F, W=50, H=37, n_layers=4)
+    G = grads_for(sc, sc.cams[0], seed=F)
+    got = gpu_run(sc, dev, G=G)
+    check_forward(sc, got)
+    check_backward(sc, got, G)
+
+
+def test_dense_tiles_multi_chunk_and_long_lists(dev):
+    """Many points in few tiles: several 512-pair chunks per tile, lists >> 16."""
+    sc = scenes.tiny_scene(11, n=30000, F=4, W=40, H=24, n_layers=3)
+    G = grads_for(sc, sc.cams[0], seed=3)
+    got = gpu_run(sc, dev, G=G)
+    check_forward(sc, got)
+    check_backward(sc, got, G)
+    assert got["stats"]["max_list"] > 100
+
+
+def test_empty_and_all_culled(dev):
+    sc = scenes.tiny_scene(1, n=10)
+    sc.pos[:, :] = np.float32(np.nan)
+    got = gpu_run(sc, dev)
+    assert not got["pyr"].any() and got["stats"]["n_culled"] == 10
+    sc0 = scenes.tiny_scene(2, n=1)
+    sc0.pos, sc0.sw, sc0.alpha, sc0.desc = sc0.pos[:0], sc0.sw[:0], sc0.alpha[:0], sc0.desc[:0]
+    got = gpu_run(sc0, dev)
+    assert not got["pyr"].any() and not got["counts"].any()
+
+
+def test_forward_is_deterministic(dev):
+    sc = scenes.tiny_scene(4, n=5000, W=64, H=48)
+    a = gpu_run(sc, dev)
+    b = gpu_run(sc, dev)
+    assert np.array_equal(a["pyr"].view(np.uint32), b["pyr"].view(np.uint32))
+
+
+def test_multi_view_accumulation(dev):
+    """Gradients of several views accumulate (+=) into one packed buffer (reading Q21)."""
+    from paper_2401_06003_b200 import Rasterizer
+    sc = scenes.make_config("C4", n=20000, n_views=3)
+    cams = [scenes.look_at(-c.R.T.astype(np.float64) @ c.t.astype(np.float64), [0, 0, 0], 160, 96, 100.0)
+            for c in sc.cams]
+    r = Rasterizer(160, 96, 4, sc.F, max_points=sc.n, device=dev)
+    pos, sw, al, de = (T(a, dev) for a in (sc.pos, sc.sw, sc.alpha, sc.desc))
+    grad = torch.zeros(sc.n, r.G, device=dev)
+    acc, accm = None, None
+    for v, cam in enumerate(cams):
+        G = scenes.grad_pyramid(r.pyramid_floats, seed=v)
+        r.project(cam, pos, sw, al, de)
+        r.forward(save=True)
+        r.backward(T(G, dev), grad)
+        acc, accm = oracle.backward(cam, 4, sc.pos, sc.sw, sc.alpha, sc.desc, G, grad=acc, grad_mag=accm)
+    gg = grad.cpu().numpy()
+    got = np.concatenate([gg[:, :5], gg[:, 5:5 + sc.F]], 1)
+    assert np.all(np.abs(got - acc) <= GRAD_TOL * accm + 1e-30)
+
+
+def test_autograd_render(dev):
+    from paper_2401_06003_b200 import Rasterizer
+    sc = scenes.c1()
+    cam = sc.cams[0]
+    r = Rasterizer(cam.width, cam.height, sc.n_layers, sc.F, max_points=sc.n, device=dev)
+    ps = [T(a, dev).requires_grad_() for a in (sc.pos, sc.sw, sc.alpha, sc.desc)]
+    layers = r.render(cam, *ps)
+    G = scenes.grad_pyramid(r.pyramid_floats, seed=7)
+    flat = torch.cat([L.reshape(-1) for L in layers])
+    (flat * T(G, dev)).sum().backward()
+    g, gm = oracle.backward(cam, sc.n_layers, sc.pos, sc.sw, sc.alpha, sc.desc, G)
+    got = np.concatenate([ps[0].grad.cpu().numpy(), ps[1].grad.cpu().numpy()[:, None],
+                          ps[2].grad.cpu().numpy()[:, None], ps[3].grad.cpu().numpy()], 1)
+    assert np.all(np.abs(got - g) <= GRAD_TOL * gm + 1e-30)
+
+
+# ------------------------------------------------------------------ ABI error paths
+
+def test_abi_error_paths(dev):
+    from paper_2401_06003_b200 import _abi as A
+    sc = scenes.c1()
+    cam = sc.cams[0]
+    plan = A.trips_plan_create(sc.n_layers, sc.F, cam.width, cam.height, sc.n)
+    try:
+        ws = torch.empty(A.trips_workspace_bytes(plan), dtype=torch.uint8, device=dev)
+        ws2 = torch.empty(A.trips_workspace_bytes(plan), dtype=torch.uint8, device=dev)
+        pyr = torch.empty(A.trips_pyramid_floats(plan), device=dev)
+        grad = torch.zeros(sc.n, A.trips_grad_stride(plan), device=dev)
+        pos, sw, al, de = (T(a, dev) for a in (sc.pos, sc.sw, sc.alpha, sc.desc))
+        args = (pos.data_ptr(), sw.data_ptr(), al.data_ptr(), de.data_ptr())
+        assert A.trips_splat_forward(plan, ws.data_ptr(), pyr.data_ptr(), 1) == A.TRIPS_ERR_STATE
+        assert A.trips_project(plan, ws.data_ptr(), cam, sc.n + 1, *args) == A.TRIPS_ERR_CAPACITY
+        assert A.trips_project(plan, ws.data_ptr() + 16, cam, sc.n, *args) == A.TRIPS_ERR_ALIGN
+        assert A.trips_project(plan, ws.data_ptr(), cam, -1, *args) == A.TRIPS_ERR_ARG
+        assert A.trips_project(plan, ws.data_ptr(), cam, sc.n, None, *args[1:]) == A.TRIPS_ERR_ARG
+        assert A.trips_project(plan, ws.data_ptr(), cam, sc.n, *args) == A.TRIPS_OK
+        assert A.trips_splat_forward(plan, ws2.data_ptr(), pyr.data_ptr(), 1) == A.TRIPS_ERR_STATE
+        assert A.trips_splat_forward(plan, ws.data_ptr(), pyr.data_ptr(), 0) == A.TRIPS_OK
+        assert A.trips_splat_backward(plan, ws.data_ptr(), pyr.data_ptr(), grad.data_ptr()) == A.TRIPS_ERR_STATE
+        assert A.trips_splat_forward(plan, ws.data_ptr(), pyr.data_ptr(), 1) == A.TRIPS_ERR_STATE  # needs project
+        assert A.trips_project(plan, ws.data_ptr(), cam, sc.n, *args) == A.TRIPS_OK
+        assert A.trips_splat_forward(plan, ws.data_ptr(), pyr.data_ptr(), 1) == A.TRIPS_OK
+        assert A.trips_splat_backward(plan, ws.data_ptr(), pyr.data_ptr(), grad.data_ptr() + 4) == A.TRIPS_ERR_ALIGN
+        assert A.trips_splat_backward(plan, ws.data_ptr(), pyr.data_ptr(), grad.data_ptr()) == A.TRIPS_OK
+        torch.cuda.synchronize()
+    finally:
+        A.trips_plan_destroy(plan)
+
+
+# ------------------------------------------------------------------ full-size configs
+
+def _sample_mask(cam, n_layers, seed, n_random=3000):
+    P = oracle.num_pixels(cam.width, cam.height, n_layers)
+    rng = np.random.default_rng(seed)
+    mask = np.zeros(P, np.uint8)
+    mask[rng.choice(P, n_random, replace=False)] = 1
+    # plus two full 16x16 blocks in layer 0 and everything in the coarsest layer
+    W = cam.width
+    for (y0, x0) in ((cam.height // 2 - 8, W // 2 - 8), (cam.height - 20, 40)):
+        for y in range(y0, y0 + 16):
+            mask[y * W + x0:y * W + x0 + 16] = 1
+    dims = oracle.layer_dims(cam.width, cam.height, n_layers)
+    mask[P - dims[-1][0] * dims[-1][1]:] = 1
+    return mask
+
+
+@pytest.mark.parametrize("name", ["C2", "C3", "C5"])
+def test_full_size_sampled(dev, name):
+    """Full-size configs in the bench launch configuration; the oracle computes sampled
+    pixels (lists restricted to a pixel mask), gradients of a loss on those pixels."""
+    sc = scenes.make_config(name)
+    cam = sc.cams[0]
+    mask = _sample_mask(cam, sc.n_layers, seed=len(name))
+    G = None if sc.forward_only else grads_for(sc, cam, seed=1, mask=mask)
+    got = gpu_run(sc, dev, G=G, save=True)
+    check_forward(sc, got, mask=mask)
+    st = got["stats"]
+    assert st["n_visible"] + st["n_culled"] == sc.n
+    assert st["n_kept"] <= st["n_frag"] and int(got["counts"].sum()) == st["n_frag"]
+    assert np.minimum(got["counts"], 16).sum() == st["n_kept"]
+    if G is not None:
+        check_backward(sc, got, G, mask=mask)
+
+
+def test_2k_relation_full_size(dev):
+    """P5 at full scale, GPU only: doubling (fx, fy, cx, cy, f, W, H) and adding a layer maps
+    layer l of the original onto layer l+1 bit for bit (counts, kept lists, features)."""
+    sc = scenes.make_config("C2", n=2_000_000)
+    cam = sc.cams[0]
+    cam.cx, cam.cy = 959.0, 539.0                      # make 2*c exact and the relation exact
+    cam2 = scenes.Camera(fx=2 * cam.fx, fy=2 * cam.fy, cx=2 * cam.cx, cy=2 * cam.cy, f=2 * cam.f, R=cam.R, t=cam.t,
+                         width=2 * cam.width, height=2 * cam.height, near=cam.near)
+    a = gpu_run(sc, dev, cam=cam)
+    sc.n_layers += 1
+    b = gpu_run(sc, dev, cam=cam2)
+    sc.n_layers -= 1
+    da = oracle.layer_dims(cam.width, cam.height, sc.n_layers)
+    db = oracle.layer_dims(cam2.width, cam2.height, sc.n_layers + 1)
+    pa = np.cumsum([0] + [h * w for h, w in da])
+    pb = np.cumsum([0] + [h * w for h, w in db])
+    F1 = sc.F + 1
+    for l in range(1, sc.n_layers):
+        assert np.array_equal(a["counts"][pa[l]:pa[l + 1]], b["counts"][pb[l + 1]:pb[l + 2]])
+        assert np.array_equal(a["kept"][pa[l]:pa[l + 1]], b["kept"][pb[l + 1]:pb[l + 2]])
+        assert np.array_equal(a["pyr"][pa[l] * F1:pa[l + 1] * F1], b["pyr"][pb[l + 1] * F1:pb[l + 2] * F1])
