@@ -1,0 +1,346 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 TRIPS rasterizer (BASELINE.json metric: forward+backward frames/s
+and splatted points/s at 1080p, HBM GB/s vs peak, 1/2/4/8-GPU scaling).
+
+Workload (BASELINE.json configs[3], "C4"): a batch of 32 camera views of an 8M-point
+Tanks&Temples-like synthetic cloud at 1920x1080, 4 pyramid layers, F = 4.  One step =
+for every view of this rank: project -> splat forward (saved) -> splat backward into
+one packed gradient buffer; then one NCCL all-reduce (SUM) of that buffer across ranks.
+Views are sharded r::N over ranks (strong scaling: the batch is fixed).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl cuda|reference]
+  torchrun --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
+
+Rank 0 prints ONE JSON line.  `--impl reference` times the CPU oracle (oracle/) on a
+bounded sample of the same workload (the one other place bench.py may execute oracle/).
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fwd+bwd frames/s and splatted points/s at 1080p; HBM GB/s vs peak; 1/2/4/8 GPU scaling"
+UNIT = "frames/s"
+N_POINTS = 8_000_000
+N_VIEWS = 32
+SAMPLE_ROWS = 4          # oracle sample: 4 strips of 32 rows (one per 1/4 band), time scaled x1080/128
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={self.FIELDS}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        self.f.seek(0)
+        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[0]))
+                mx.append(float(r[1]))
+                for k, nm in enumerate(names):
+                    if r[4 + k].strip().lower() == "active":
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                continue
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ algorithmic bytes
+
+def alg_bytes(st, n, F, P):
+    """Compulsory DRAM bytes per view and kernel.
+    st: trips stats of the view (n_visible, n_pairs, n_frag, n_kept)."""
+    nv, npairs, nk = st["n_visible"], st["n_pairs"], st["n_kept"]
+    G = 8 + 4 * ((F + 3) // 4)
+    rec = 4 * (4 + 4 * ((F + 3) // 4)) + 4                    # screen record + z
+    k = {}
+    k["project"] = (16 + 4 + 4 * F) * n + rec * n              # read pos,s_w,alpha,tau; write record
+    k["bin"] = 16 * n + 4 * npairs                             # read (x,y,s); write bin entries
+    k["raster"] = 4 * npairs + (20 + 4 * F) * nv + 4 * (F + 1) * P + 8 * nk + 8 * P
+    k["backward"] = 8 * nk + 4 * P + 4 * (F + 1) * P + (20 + 4 * F) * nv + 2 * 4 * G * nv
+    k["scan"] = 0
+    return k
+
+
+# ------------------------------------------------------------------ CPU oracle sample
+
+def oracle_sample(sc, cam, rows=SAMPLE_ROWS, phase=0, seed=100, strip=32):
+    """One view forward+backward of the oracle on `rows` horizontal strips of `strip` pixel rows,
+    one strip per 1/`rows` band of the image, each a crop camera (same intrinsics, cy shifted by
+    a multiple of 2^(n-1) so every layer's pixel grid is the full image's) over the points that
+    can reach it (a generous numpy pre-filter; sample selection only).  Returns the oracle's
+    seconds scaled by H / (rows * strip), the pixel fraction."""
+    from oracle import oracle
+    from synth import scenes
+    H = cam.height
+    band = H // rows
+    align = 1 << (sc.n_layers - 1)
+    p = sc.pos.astype(np.float64) @ cam.R.astype(np.float64).T + cam.t.astype(np.float64)
+    total = 0.0
+    for b in range(rows):
+        y0 = (b * band + (phase * 37) % max(band - strip, 1)) // align * align
+        crop = scenes.Camera(fx=cam.fx, fy=cam.fy, cx=cam.cx, cy=cam.cy - y0, f=cam.f, R=cam.R, t=cam.t,
+                             width=cam.width, height=strip, near=cam.near)
+        with np.errstate(all="ignore"):
+            u = cam.fx * p[:, 0] / p[:, 2] + cam.cx
+            v = cam.fy * p[:, 1] / p[:, 2] + crop.cy
+            margin = 64 + 2 * cam.f * sc.sw / p[:, 2]
+            keep = (p[:, 2] > cam.near) & (u > -margin) & (u < cam.width + margin) & (v > -margin) & \
+                (v < strip + margin)
+        idx = np.nonzero(keep)[0]
+        pos, sw, al, de = sc.pos[idx], sc.sw[idx], sc.alpha[idx], sc.desc[idx]
+        P = oracle.num_pixels(crop.width, crop.height, sc.n_layers)
+        G = scenes.grad_pyramid(P * (sc.F + 1), seed=seed + b)
+        t0 = time.perf_counter()
+        oracle.forward(crop, sc.n_layers, pos, sw, al, de, want_kept=False)
+        oracle.backward(crop, sc.n_layers, pos, sw, al, de, G)
+        total += time.perf_counter() - t0
+    return total * H / (rows * strip)
+
+
+def run_reference(args, rank, world):
+    from synth import scenes
+    if rank != 0:
+        return
+    sc = scenes.make_config("C4", n=N_POINTS, n_views=N_VIEWS, order=args.order)
+    for w in range(args.warmup):
+        oracle_sample(sc, sc.cams[w % N_VIEWS], phase=w)
+    times = [oracle_sample(sc, sc.cams[(args.warmup + k) % N_VIEWS], phase=k) for k in range(args.steps)]
+    t_view = sum(times) / len(times)                  # seconds per full view (scaled)
+    value = 1.0 / t_view
+    sample = ("per step: 1 view of C4 (8M points, 1920x1080, n=4, F=4), oracle forward+backward on 4 strips "
+              "of 32 pixel rows (one per 1/4 band; crop cameras over the points that can reach them), "
+              "time x1080/128; single thread")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_view * 1e3 * N_VIEWS,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "config": {"workload": "C4: 32 views x 8M points, 1920x1080, 4 layers, F=4",
+                                             "point_order": args.order},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ CUDA arm
+
+def run_cuda(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2401_06003_b200 import Rasterizer, _abi
+    from synth import scenes
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    sc = scenes.make_config("C4", n=N_POINTS, n_views=N_VIEWS, order=args.order)
+    n, F = sc.n, sc.F
+    W, H = sc.cams[0].width, sc.cams[0].height
+    rast = Rasterizer(W, H, sc.n_layers, F, max_points=n, device=dev)
+    host = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory()
+            for k, v in (("pos", sc.pos), ("sw", sc.sw), ("alpha", sc.alpha), ("desc", sc.desc))}
+    d = {k: v.to(dev, non_blocking=True) for k, v in host.items()}
+    Gp = torch.from_numpy(scenes.grad_pyramid(rast.pyramid_floats, seed=100)).to(dev)
+    grad = torch.zeros(n, rast.G, dtype=torch.float32, device=dev)
+    my_views = list(range(rank, N_VIEWS, world))
+    stream = torch.cuda.current_stream()
+
+    def step(dv, grad_buf):
+        grad_buf.zero_()
+        for v in my_views:
+            rast.project(sc.cams[v], dv["pos"], dv["sw"], dv["alpha"], dv["desc"])
+            rast.forward(save=True)
+            rast.backward(Gp, grad_buf)
+        if world > 1:
+            dist.all_reduce(grad_buf, op=dist.ReduceOp.SUM)
+
+    # per-view statistics (deterministic; read outside the timed region)
+    view_stats = []
+    for v in my_views:
+        rast.project(sc.cams[v], d["pos"], d["sw"], d["alpha"], d["desc"])
+        rast.forward(save=True)
+        view_stats.append(rast.stats())
+    torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step(d, grad)
+    torch.cuda.synchronize()
+
+    # ---- device-timed region: inputs resident in HBM
+    rast.stage_ms(reset=True)
+    rast.set_profiling(True)
+    l0 = _abi.trips_launch_count()
+    clocks = ClockSampler(local_rank)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step(d, grad)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    launches = _abi.trips_launch_count() - l0
+    rast.set_profiling(False)
+    stage = rast.stage_ms(reset=True)
+    ms = e0.elapsed_time(e1)
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+
+    # ---- end to end through the public API: pinned host inputs in, gradients out
+    out_host = torch.empty(n, rast.G, dtype=torch.float32).pin_memory()
+    h2d = sum(v.numel() * v.element_size() for v in host.values())
+    d2h = out_host.numel() * out_host.element_size()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for _ in range(args.steps):
+        dv = {k: v.to(dev, non_blocking=True) for k, v in host.items()}
+        step(dv, grad)
+        out_host.copy_(grad, non_blocking=True)
+    f1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    e2e_ms = float(e2e_ms.item())
+
+    # ---- roofline of the dominant kernel (stage events are on the launching stream)
+    peak, peak_src = peaks()
+    per_view_bytes = [alg_bytes(s, n, F, rast.P) for s in view_stats]
+    stage_ms = {k: v[0] for k, v in stage.items()}
+    stage_launch = {k: v[1] for k, v in stage.items()}
+    dom = max(("raster", "backward", "project", "bin"), key=lambda k: stage_ms[k])
+    dom_launch_ms = stage_ms[dom] / max(stage_launch[dom], 1)
+    dom_bytes = sum(b[dom] for b in per_view_bytes) / len(per_view_bytes)
+    achieved = dom_bytes / (dom_launch_ms * 1e-3) / 1e9
+    step_bytes = sum(sum(b.values()) for b in per_view_bytes)
+    step_ms = ms_max / args.steps
+
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "dram_traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get(dom)
+        except Exception:
+            traffic = None
+
+    if rank == 0:
+        value = N_VIEWS / (step_ms * 1e-3)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "C4: batch of 32 views x 8M points (T&T-like), 1920x1080, 4 layers, F=4, "
+                                   "fwd+bwd, view-parallel + NCCL all-reduce of point gradients",
+                       "global_batch": N_VIEWS, "points": n, "resolution": [W, H], "layers": sc.n_layers,
+                       "features": F, "parallelism": f"views{world}", "point_order": args.order,
+                       "l2": "inputs larger than L2 (288 MB of point data, 384 MB gradients per step)"},
+            "points_per_s": N_VIEWS * n / (step_ms * 1e-3),
+            "fragments_per_s": sum(s["n_frag"] for s in view_stats) * world / (step_ms * 1e-3),
+            "alg_GBps_step": step_bytes * world / (step_ms * 1e-3) / 1e9,
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "alg_bytes_per_launch": dom_bytes, "launch_ms": dom_launch_ms},
+            "stage_ms_per_step": {k: v / args.steps for k, v in stage_ms.items()},
+            "gpu_launches": launches,
+            "gpu_launches_per_step": launches / args.steps,
+            "e2e": {"value": N_VIEWS / (e2e_ms / args.steps * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "view_stats_mean": {k: float(np.mean([s[k] for s in view_stats])) for k in view_stats[0]},
+        }
+        if clk is not None:
+            line["clocks"] = clk
+        if world == 1 and not args.no_cpu_baseline:
+            from oracle import oracle as _o  # noqa: F401  (cpu_baseline leg only)
+            t = [oracle_sample(sc, sc.cams[k], phase=k + 3) for k in range(2)]
+            v = 1.0 / (sum(t) / len(t))
+            line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                                    "sample": "2 views of C4 (8M points), oracle fwd+bwd on 4 strips of 32 pixel "
+                                              "rows each (one per 1/4 band, crop cameras), time x1080/128; "
+                                              "single thread"}
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
+    ap.add_argument("--order", default="random", choices=["random", "morton"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    run_cuda(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
