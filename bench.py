@@ -98,13 +98,13 @@ def alg_bytes(st, n, F, P):
     st: trips stats of the view (n_visible, n_pairs, n_frag, n_kept)."""
     nv, npairs, nk = st["n_visible"], st["n_pairs"], st["n_kept"]
     G = 8 + 4 * ((F + 3) // 4)
-    rec = 4 * (4 + 4 * ((F + 3) // 4)) + 4                    # screen record + z
+    rec = 16 + 4 * F                                           # screen record (x, y, s, alpha, tau)
     k = {}
-    k["project"] = (16 + 4 + 4 * F) * n + rec * n              # read pos,s_w,alpha,tau; write record
-    k["bin"] = 16 * n + 4 * npairs                             # read (x,y,s); write bin entries
-    k["raster"] = 4 * npairs + (20 + 4 * F) * nv + 4 * (F + 1) * P + 8 * nk + 8 * P
-    k["backward"] = 8 * nk + 4 * P + 4 * (F + 1) * P + (20 + 4 * F) * nv + 2 * 4 * G * nv
-    k["scan"] = 0
+    k["count"] = 16 * n                                        # read pos, s_w
+    k["emit"] = (16 + 4 + 4 * F) * n + rec * n + 12 * npairs   # read inputs; write record + pairs
+    k["sort"] = 2 * (12 + 12 + 4) * npairs                     # 2 radix passes: histogram + move
+    k["raster"] = 12 * npairs + rec * nv + 4 * (F + 1) * P + 8 * nk + 8 * P
+    k["backward"] = 8 * nk + 4 * P + 4 * (F + 1) * P + rec * nv + 2 * 4 * G * nv
     return k
 
 
@@ -262,7 +262,7 @@ def run_cuda(args, rank, world, local_rank):
     per_view_bytes = [alg_bytes(s, n, F, rast.P) for s in view_stats]
     stage_ms = {k: v[0] for k, v in stage.items()}
     stage_launch = {k: v[1] for k, v in stage.items()}
-    dom = max(("raster", "backward", "project", "bin"), key=lambda k: stage_ms[k])
+    dom = max(("raster", "backward"), key=lambda k: stage_ms[k])     # single-kernel stages
     dom_launch_ms = stage_ms[dom] / max(stage_launch[dom], 1)
     dom_bytes = sum(b[dom] for b in per_view_bytes) / len(per_view_bytes)
     achieved = dom_bytes / (dom_launch_ms * 1e-3) / 1e9

@@ -163,7 +163,7 @@ int trips_read_stats(const trips_plan* plan, const void* ws, trips_stats* out, v
 int trips_debug_export(const trips_plan* plan, const void* ws, int32_t what, void* dst, void* stream);
 
 /* Per-stage device timing.  When enabled, CUDA events bracket every kernel stage
- * (0 project, 1 scan, 2 bin, 3 raster, 4 backward); trips_read_stage_ms synchronises
+ * (0 count, 1 emit, 2 sort, 3 raster, 4 backward); trips_read_stage_ms synchronises
  * the events and returns the accumulated milliseconds and launch counts since the last
  * reset.  Returns the number of stages written. */
 int trips_set_profiling(trips_plan* plan, int32_t enable);

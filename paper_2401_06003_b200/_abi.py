@@ -21,7 +21,7 @@ TRIPS_FWD_SAVE_FOR_BACKWARD = 1
 TRIPS_EXPORT_COUNTS = 1
 TRIPS_EXPORT_KEPT = 2
 N_STAGES = 5
-STAGE_NAMES = ("project", "scan", "bin", "raster", "backward")
+STAGE_NAMES = ("count", "emit", "sort", "raster", "backward")
 
 
 class trips_camera(C.Structure):

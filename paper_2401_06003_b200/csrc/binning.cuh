@@ -1,0 +1,222 @@
+// binning.cuh -- "collecting" and "splatting" without global atomics.
+//
+// The paper counts fragments per pixel with atomics, scans the counts and fills per-pixel
+// lists.  On B200 the per-pixel (or per-tile) global atomic counters are the bottleneck for
+// randomly ordered clouds: thousands of same-address atomics per hot tile serialise in L2.
+// This build privatises the counters instead.  A persistent grid of C CTAs splits the points
+// into C contiguous ranges; every CTA keeps one counter per pyramid tile in shared memory:
+//
+//   k_count  per CTA: project its points (Sec. 3.1, Eq. 2), enumerate their (point, tile)
+//            pairs (Eq. 4 layers, 2x2 footprints), count them per tile in shared memory;
+//            then reserve its slice of each touched tile with ONE global atomic per (CTA,
+//            tile) on the tile total; the returned base goes to hist[c][t]
+//   k_tscan  one CTA: exclusive scan of the tile totals -> tile_off; kept-list capacity base
+//   k_emit   per CTA, same point range: project again (bit-identical), write the screen
+//            record, place every pair at tile_off[t] + hist[c][t] + (shared-memory cursor)
+//
+// The order of pairs inside a tile's bin is not defined; K4 orders fragments by the full
+// (z, i) key (reading Q12), so results do not depend on it.
+#pragma once
+#include "common.cuh"
+
+namespace trips {
+
+constexpr int kBinThreads = 512;           // threads per binning CTA
+constexpr int kBinCtasPerSm = 3;
+constexpr int kMaxTilesSmem = 49152;       // 192 KB of shared-memory counters
+
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+
+// Block-wide exclusive scan of one u32 per thread (any multiple of 32 threads <= 1024).
+// Returns the exclusive prefix; *total receives the block sum.  `warp_sums` >= 32 u32.
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* warp_sums, uint32_t* total)
+{
+    const unsigned lane = lane_id(), warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= (unsigned)o) x += y;
+    }
+    if (lane == 31) warp_sums[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t w = lane < nw ? warp_sums[lane] : 0u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= (unsigned)o) w += y;
+        }
+        warp_sums[lane] = w;                 // inclusive warp prefixes
+    }
+    __syncthreads();
+    const uint32_t wpre = warp ? warp_sums[warp - 1] : 0u;
+    *total = warp_sums[nw - 1];
+    __syncthreads();                         // warp_sums may be reused by the caller
+    return wpre + x - v;
+}
+
+// The CTA's contiguous point range [b, e).
+__device__ __forceinline__ void cta_range(int n, int& b, int& e)
+{
+    const int per = (n + gridDim.x - 1) / gridDim.x;
+    b = min(n, (int)blockIdx.x * per);
+    e = min(n, b + per);
+}
+
+// --------------------------------------------------------------------------- k_count
+
+__global__ void __launch_bounds__(kBinThreads) k_count(Params P)
+{
+    extern __shared__ __align__(16) uint32_t s_hist[];            // [T]
+    __shared__ uint32_t s_v;
+    for (int t = threadIdx.x; t < P.T; t += blockDim.x) s_hist[t] = 0;
+    if (threadIdx.x == 0) s_v = 0;
+    __syncthreads();
+    int b, e;
+    cta_range(P.n, b, e);
+    uint32_t nvis = 0;
+    for (int i = b + threadIdx.x; i < e; i += blockDim.x) {
+        const float* q = P.pos + 3 * (size_t)i;
+        float xs, ys, z, s;
+        if (project_exact(P.cam, __ldg(q), __ldg(q + 1), __ldg(q + 2), __ldg(P.sw + i), xs, ys, z, s)) {
+            ++nvis;
+            const PointPairs pp = point_pairs(P, xs, ys, s);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                uint32_t o;
+                const int t = pair_slot(P, pp, k, o);
+                if (t >= 0) atomicAdd(&s_hist[t], 1u);
+            }
+        }
+    }
+    const uint32_t wv = __reduce_add_sync(0xffffffffu, nvis);
+    if (lane_id() == 0 && wv) atomicAdd(&s_v, wv);
+    __syncthreads();
+    // reserve this CTA's slice of every tile it touches: tile_off[t] holds the running tile
+    // total here (k_tscan turns totals into offsets); the returned value is the CTA's offset
+    // inside the tile.  One atomic per (CTA, non-empty tile), spread over T addresses.
+    uint32_t* row = P.hist + (size_t)blockIdx.x * P.T;
+    for (int t = threadIdx.x; t < P.T; t += blockDim.x) {
+        const uint32_t c = s_hist[t];
+        if (c) row[t] = atomicAdd(&P.tile_off[t], c);
+    }
+    if (threadIdx.x == 0) P.cta_vis[blockIdx.x] = s_v;
+}
+
+// --------------------------------------------------------------------------- k_tscan
+
+// One CTA: tile_off <- exclusive scan of the tile totals (tile_off[T] = M); tile_kbase <-
+// exclusive scan of the kept-list capacity min(16 * 256, 4 * pairs(t)).
+__global__ void __launch_bounds__(1024) k_tscan(Params P)
+{
+    __shared__ uint32_t s_ws[32];
+    const int T = P.T;
+    uint32_t ca = 0, cb = 0;
+    for (int base = 0; base < T; base += blockDim.x) {
+        const int t = base + threadIdx.x;
+        const uint32_t a = t < T ? P.tile_off[t] : 0u;
+        const uint32_t b = min(4u * a, (uint32_t)(kTilePix * kCap));
+        uint32_t ta, tb;
+        const uint32_t pa = block_excl_scan(a, s_ws, &ta);
+        const uint32_t pb = block_excl_scan(t < T ? b : 0u, s_ws, &tb);
+        if (t < T) {
+            P.tile_off[t] = ca + pa;
+            P.tile_kbase[t] = cb + pb;
+        }
+        ca += ta;
+        cb += tb;
+    }
+    if (threadIdx.x == 0) {
+        P.tile_off[T] = ca;
+        P.tile_kbase[T] = cb;
+    }
+}
+
+// --------------------------------------------------------------------------- k_emit
+
+template <int FC>
+__global__ void __launch_bounds__(kBinThreads) k_emit(Params P, int8_t* __restrict__ level_out,
+                                                      float* __restrict__ proj_out)
+{
+    extern __shared__ __align__(16) uint32_t s_cur[];             // [T] fill cursors
+    const uint32_t* row = P.hist + (size_t)blockIdx.x * P.T;
+    for (int t = threadIdx.x; t < P.T; t += blockDim.x) s_cur[t] = P.tile_off[t] + row[t];   // garbage for tiles
+                                                                  // this CTA never touches
+    __syncthreads();
+    int b, e;
+    cta_range(P.n, b, e);
+    for (int i = b + threadIdx.x; i < e; i += blockDim.x) {
+        float xs = 0.f, ys = 0.f, z = 0.f, s = 0.f;
+        const float* q = P.pos + 3 * (size_t)i;
+        const bool vis = project_exact(P.cam, __ldg(q), __ldg(q + 1), __ldg(q + 2), __ldg(P.sw + i), xs, ys, z, s);
+        float4* r = reinterpret_cast<float4*>(P.rec + (size_t)i * P.RS);
+        r[0] = make_float4(vis ? xs : 0.f, vis ? ys : 0.f, vis ? s : kCulled, __ldg(P.alpha + i));
+        const float* d = P.desc + (size_t)i * P.F;
+        if (P.F == FC && (reinterpret_cast<uintptr_t>(d) & 15) == 0) {
+#pragma unroll
+            for (int c = 0; c < FC / 4; ++c) r[1 + c] = __ldg(reinterpret_cast<const float4*>(d) + c);
+        } else {
+#pragma unroll
+            for (int c = 0; c < FC / 4; ++c) {
+                float v[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) v[j] = (4 * c + j < P.F) ? __ldg(d + 4 * c + j) : 0.f;
+                r[1 + c] = make_float4(v[0], v[1], v[2], v[3]);
+            }
+        }
+        if (level_out) level_out[i] = (int8_t)(vis ? select_levels(s, P.n_layers).code : -1);
+        if (proj_out) {
+            const float nan = __int_as_float(0x7fc00000);
+            reinterpret_cast<float4*>(proj_out)[i] = vis ? make_float4(xs, ys, z, s) : make_float4(nan, nan, nan, nan);
+        }
+        if (!vis) continue;
+        const uint64_t key = ((uint64_t)__float_as_uint(z) << 32) | (uint32_t)i;
+        const PointPairs pp = point_pairs(P, xs, ys, s);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            uint32_t o;
+            const int t = pair_slot(P, pp, k, o);
+            if (t >= 0) {
+                const uint32_t pos = atomicAdd(&s_cur[t], 1u);
+                P.bin_key[pos] = key;
+                P.bin_orig[pos] = (uint16_t)o;
+            }
+        }
+    }
+}
+
+// --------------------------------------------------------------------------- k_stats
+
+// On-demand statistics (trips_read_stats): reduces the per-pixel list lengths and the
+// per-CTA visible counts; nothing on the hot path touches a shared counter.
+__global__ void __launch_bounds__(256) k_stats(Params P, int ctas, int npix)
+{
+    unsigned long long frag = 0, kept = 0, trunc = 0, mx = 0, vis = 0;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < npix; j += gridDim.x * blockDim.x) {
+        const unsigned long long c = P.pix_cnt[j];
+        frag += c;
+        kept += c < (unsigned long long)kCap ? c : (unsigned long long)kCap;
+        trunc += c > (unsigned long long)kCap;
+        mx = c > mx ? c : mx;
+    }
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < ctas; j += gridDim.x * blockDim.x) vis += P.cta_vis[j];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        frag += __shfl_xor_sync(0xffffffffu, frag, o);
+        kept += __shfl_xor_sync(0xffffffffu, kept, o);
+        trunc += __shfl_xor_sync(0xffffffffu, trunc, o);
+        vis += __shfl_xor_sync(0xffffffffu, vis, o);
+        const unsigned long long m2 = __shfl_xor_sync(0xffffffffu, mx, o);
+        mx = m2 > mx ? m2 : mx;
+    }
+    if (lane_id() == 0) {
+        if (frag) atomicAdd(&P.stats[S_FRAG], frag);
+        if (kept) atomicAdd(&P.stats[S_KEPT], kept);
+        if (trunc) atomicAdd(&P.stats[S_TRUNC], trunc);
+        if (vis) atomicAdd(&P.stats[S_VISIBLE], vis);
+        if (mx) atomicMax(&P.stats[S_MAXLIST], mx);
+    }
+}
+
+}  // namespace trips

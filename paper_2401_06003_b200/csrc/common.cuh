@@ -45,15 +45,16 @@ struct Params {
     const float* pos; const float* sw; const float* alpha; const float* desc;
     // workspace
     float* rec;            // [n][RS]  (x, y, s, alpha, tau[FC])     s < 0 marks culled
-    float* zbuf;           // [n]      view depth z
-    uint32_t* tile_cnt;    // [T]      (point, tile) pairs per tile
-    uint32_t* tile_off;    // [T+1]    exclusive scan of tile_cnt
-    uint32_t* tile_cur;    // [T]      fill cursors
+    uint32_t* hist;        // [C][T]   per-CTA tile counts -> per-CTA offsets within the tile
+    uint32_t* cta_vis;     // [C]      visible points per binning CTA (statistics)
+    uint32_t* tile_off;    // [T+1]    first pair of each tile's bin; [T] = number of pairs M
     uint32_t* tile_kbase;  // [T+1]    kept-list base per tile (scan of min(4096, 4 cnt))
-    uint32_t* bins;        // [8n]     point index per (tile, pair)
+    uint64_t* bin_key;     // [8n]     (z bits << 32 | i) per (tile, pair), tile-major
+    uint16_t* bin_orig;    // [8n]     footprint origin in the tile: (qx0+1) | (qy0+1) << 5
     uint32_t* pix_cnt;     // [T*256]  list length per tile pixel
     uint32_t* pix_meta;    // [T*256]  (local kept offset << 5) | K
     uint64_t* kept;        // [kcap]   kept (z, i) keys, per pixel in blend order
+    float* kept_gamma;     // [kcap]   gamma of each kept fragment (saved for the backward)
     unsigned long long* stats;  // [8]  n_culled, n_visible, n_pairs, n_frag, n_kept, n_trunc, max_list
 };
 
@@ -150,16 +151,27 @@ __device__ __forceinline__ bool footprint(float xs, float ys, int l, int Wl, int
 
 // (point, tile) pairs of a point: for each selected layer the tiles touched by the
 // in-bounds pixels of its 2x2 footprint.  Deterministic in (xs, ys, s) so K1 (count) and
-// K3 (fill) enumerate identical lists.  Returns the count (<= 8); optionally the number
-// of in-bounds footprint pixels (= fragments of the point).
-__device__ __forceinline__ int enumerate_pairs(const Params& P, float xs, float ys, float s,
-                                               int tiles[8], int* n_frag)
+// K3 (fill) enumerate identical pairs.  Fixed slots k = 4*layer_sel + 2*dy + dx (no
+// dynamic register indexing): slot k is valid iff layer_sel exists, its footprint has
+// in-bounds pixels, and the footprint crosses a tile border in x (dx) / y (dy) if set.
+struct PointPairs {
+    int layer[2];          // layer id, -1 if absent / footprint fully out of bounds
+    int x0[2], y0[2];      // footprint origin (floor(x_l), floor(y_l))
+    int tx0[2], ty0[2];    // tile of the first in-bounds footprint pixel
+    int sx[2], sy[2];      // 1 if the in-bounds footprint spans two tiles in x / y
+    int nfrag;             // in-bounds footprint pixels over both layers (= fragments)
+};
+
+__device__ __forceinline__ PointPairs point_pairs(const Params& P, float xs, float ys, float s)
 {
-    int np = 0, nf = 0;
+    PointPairs pp;
+    pp.nfrag = 0;
     const Levels lv = select_levels(s, P.n_layers);
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
-        if (k >= lv.n) break;
+        pp.layer[k] = -1;
+        pp.x0[k] = pp.y0[k] = pp.tx0[k] = pp.ty0[k] = pp.sx[k] = pp.sy[k] = 0;
+        if (k >= lv.n) continue;
         const int l = lv.lo + k;
         const LayerGeom& G = P.L[l];
         Foot f;
@@ -167,13 +179,27 @@ __device__ __forceinline__ int enumerate_pairs(const Params& P, float xs, float 
         const int xa = max(f.x0, 0), xb = min(f.x0 + 1, G.W - 1);
         const int ya = max(f.y0, 0), yb = min(f.y0 + 1, G.H - 1);
         if (xa > xb || ya > yb) continue;
-        nf += (xb - xa + 1) * (yb - ya + 1);
-        const int tx0 = xa >> 4, tx1 = xb >> 4, ty0 = ya >> 4, ty1 = yb >> 4;
-        for (int ty = ty0; ty <= ty1; ++ty)
-            for (int tx = tx0; tx <= tx1; ++tx) tiles[np++] = G.tile_base + ty * G.tiles_x + tx;
+        pp.layer[k] = l;
+        pp.x0[k] = f.x0; pp.y0[k] = f.y0;
+        pp.tx0[k] = xa >> 4; pp.ty0[k] = ya >> 4;
+        pp.sx[k] = (xb >> 4) != (xa >> 4);
+        pp.sy[k] = (yb >> 4) != (ya >> 4);
+        pp.nfrag += (xb - xa + 1) * (yb - ya + 1);
     }
-    if (n_frag) *n_frag = nf;
-    return np;
+    return pp;
+}
+
+// Slot k of a point: returns the global tile id (or -1) and the footprint origin relative
+// to that tile, packed as (qx0 + 1) | (qy0 + 1) << 5 with qx0, qy0 in [-1, 15].
+__device__ __forceinline__ int pair_slot(const Params& P, const PointPairs& pp, int k, uint32_t& orig)
+{
+    const int ls = k >> 2, dy = (k >> 1) & 1, dx = k & 1;
+    const int l = pp.layer[ls];
+    if (l < 0 || (dx && !pp.sx[ls]) || (dy && !pp.sy[ls])) return -1;
+    const LayerGeom& G = P.L[l];
+    const int tx = pp.tx0[ls] + dx, ty = pp.ty0[ls] + dy;
+    orig = (uint32_t)(pp.x0[ls] - tx * 16 + 1) | ((uint32_t)(pp.y0[ls] - ty * 16 + 1) << 5);
+    return G.tile_base + ty * G.tiles_x + tx;
 }
 
 // u64 compare-exchange: (a, b) <- (min, max)

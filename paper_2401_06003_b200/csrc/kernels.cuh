@@ -1,36 +1,23 @@
-// kernels.cuh -- the five kernels of the B200 TRIPS rasterizer.
+// kernels.cuh -- rasterization and backward kernels of the B200 TRIPS rasterizer
+// (DESIGN.md "Kernels"); binning.cuh holds the collecting/splatting stages.
 //
-//   K1 k_project   per point: Sec. 3.1 projection + Eq. (2) size + Eq. (4) layers, writes the
-//                  point's 16-B-aligned screen record, counts (point, tile) pairs per 16x16
-//                  pyramid tile with warp-aggregated atomics.          ("collecting")
-//   K2 k_scan      one CTA: exclusive scan of the per-tile pair counts (and of the per-tile
-//                  kept-list capacity).                                ("offset scan")
-//   K3 k_bin       per point: same pair enumeration, warp-aggregated cursor atomics, writes the
-//                  point index into its tiles' bins.                   ("splatting")
-//   K4 k_raster    per tile (CTA of 256 = 16x16 pixel threads): stages chunks of the tile's
-//                  points, builds the per-pixel fragment lists in shared memory (counting sort
-//                  by pixel), keeps the 16 smallest (z, i) keys per pixel in registers with
-//                  sorting/merging networks, then blends front to back and stores the sorted
-//                  kept lists.                     ("combined sorting and accumulation", 290-295)
-//   K5 k_backward  per tile pixel: replays the kept list (forward for T_m, then reverse suffix
-//                  recurrences), chains screen-space gradients to world space per fragment and
-//                  accumulates with 16-byte vector reductions (red.global.add.v4.f32).
+//   k_raster   per tile (CTA of 256 = 16x16 pixel threads): streams the tile's (point, tile)
+//              pairs in chunks, builds the per-pixel fragment lists in shared memory
+//              (counting sort by pixel), keeps the 16 smallest (z, i) keys per pixel in
+//              registers with Batcher odd-even sorting/merging networks, blends front to back
+//              and stores the sorted kept lists and their gamma.
+//                                                 ("combined sorting and accumulation", 290-295)
+//   k_backward per tile pixel: T_m from the saved gamma_m, reverse replay with suffix
+//              recurrences, screen -> world chain per fragment, 16-byte vector reductions
+//              (red.global.add.v4.f32) into the packed gradient rows.
 #pragma once
-#include "common.cuh"
+#include "binning.cuh"
 
 namespace trips {
 
 constexpr int kChunk = 512;                 // (point, tile) pairs staged per K4 iteration
 constexpr int kPairsPerThread = kChunk / kTilePix;
-
-__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
-
-__device__ __forceinline__ unsigned lanemask_lt()
-{
-    unsigned m;
-    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
-    return m;
-}
+constexpr int kBatch = 4;                   // record gathers issued together (memory-level parallelism)
 
 __device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d)
 {
@@ -38,197 +25,55 @@ __device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float 
                  :: "l"(addr), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
 }
 
-// Block-wide exclusive scan of one u32 per thread (256 threads).  Returns the exclusive
-// prefix; *total receives the block sum.  Uses `warp_sums` (>= 8 u32 of shared memory).
-__device__ __forceinline__ uint32_t block_excl_scan256(uint32_t v, uint32_t* warp_sums, uint32_t* total)
+// --------------------------------------------------------------------------- networks
+
+// Batcher odd-even merge sort networks (ascending), verified exhaustively with the 0-1
+// principle (tests/test_networks.py): 19 comparators for 8 keys, 63 for 16.
+template <int N>
+__device__ __forceinline__ void sort_small(uint64_t (&t)[16]);
+
+template <>
+__device__ __forceinline__ void sort_small<8>(uint64_t (&t)[16])
 {
-    const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
-    uint32_t x = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= (unsigned)o) x += y;
-    }
-    if (lane == 31) warp_sums[warp] = x;
-    __syncthreads();
-    uint32_t wpre = 0, tot = 0;
-#pragma unroll
-    for (int w = 0; w < kTilePix / 32; ++w) {
-        const uint32_t ws = warp_sums[w];
-        wpre += (w < (int)warp) ? ws : 0u;
-        tot += ws;
-    }
-    __syncthreads();                        // warp_sums may be reused by the caller
-    *total = tot;
-    return wpre + x - v;
+    cswap(t[0], t[1]); cswap(t[2], t[3]); cswap(t[0], t[2]); cswap(t[1], t[3]); cswap(t[1], t[2]);
+    cswap(t[4], t[5]); cswap(t[6], t[7]); cswap(t[4], t[6]); cswap(t[5], t[7]); cswap(t[5], t[6]);
+    cswap(t[0], t[4]); cswap(t[2], t[6]); cswap(t[2], t[4]); cswap(t[1], t[5]); cswap(t[3], t[7]);
+    cswap(t[3], t[5]); cswap(t[1], t[2]); cswap(t[3], t[4]); cswap(t[5], t[6]);
 }
 
-// --------------------------------------------------------------------------- K1 project
-
-template <int FC>
-__global__ void __launch_bounds__(256) k_project(Params P, int8_t* __restrict__ level_out,
-                                                 float* __restrict__ proj_out)
+template <>
+__device__ __forceinline__ void sort_small<16>(uint64_t (&t)[16])
 {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    const bool in = i < P.n;
-    int tiles[8];
-    int np = 0, nf = 0;
-    bool vis = false;
-    if (in) {
-        const float X = P.pos[3 * (size_t)i + 0], Y = P.pos[3 * (size_t)i + 1], Z = P.pos[3 * (size_t)i + 2];
-        const float sw = P.sw[i];
-        float xs = 0.f, ys = 0.f, z = 0.f, s = 0.f;
-        vis = project_exact(P.cam, X, Y, Z, sw, xs, ys, z, s);
-        int code = -1;
-        if (vis) {
-            np = enumerate_pairs(P, xs, ys, s, tiles, &nf);
-            code = select_levels(s, P.n_layers).code;
-        }
-        float4* r = reinterpret_cast<float4*>(P.rec + (size_t)i * P.RS);
-        r[0] = make_float4(vis ? xs : 0.f, vis ? ys : 0.f, vis ? s : kCulled, P.alpha[i]);
-        const float* d = P.desc + (size_t)i * P.F;
-#pragma unroll
-        for (int c = 0; c < FC / 4; ++c) {
-            float v[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) v[j] = (4 * c + j < P.F) ? d[4 * c + j] : 0.f;
-            r[1 + c] = make_float4(v[0], v[1], v[2], v[3]);
-        }
-        P.zbuf[i] = vis ? z : __int_as_float(0x7f800000);
-        if (level_out) level_out[i] = (int8_t)code;
-        if (proj_out) {
-            const float nan = __int_as_float(0x7fc00000);
-            reinterpret_cast<float4*>(proj_out)[i] = vis ? make_float4(xs, ys, z, s) : make_float4(nan, nan, nan, nan);
-        }
-    }
-    // warp-aggregated per-tile pair counts
-    const unsigned lane = lane_id();
-    const int wmax = __reduce_max_sync(0xffffffffu, np);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        if (k >= wmax) break;
-        const int t = k < np ? tiles[k] : -1;
-        const unsigned peers = __match_any_sync(0xffffffffu, t);
-        if (t >= 0 && lane == (unsigned)(__ffs(peers) - 1)) atomicAdd(&P.tile_cnt[t], (uint32_t)__popc(peers));
-    }
-    // statistics
-    const unsigned nvis = __popc(__ballot_sync(0xffffffffu, in && vis));
-    const unsigned ncul = __popc(__ballot_sync(0xffffffffu, in && !vis));
-    if (lane == 0) {
-        if (nvis) atomicAdd(&P.stats[S_VISIBLE], (unsigned long long)nvis);
-        if (ncul) atomicAdd(&P.stats[S_CULLED], (unsigned long long)ncul);
-    }
+    cswap(t[0], t[1]); cswap(t[2], t[3]); cswap(t[0], t[2]); cswap(t[1], t[3]); cswap(t[1], t[2]);
+    cswap(t[4], t[5]); cswap(t[6], t[7]); cswap(t[4], t[6]); cswap(t[5], t[7]); cswap(t[5], t[6]);
+    cswap(t[0], t[4]); cswap(t[2], t[6]); cswap(t[2], t[4]); cswap(t[1], t[5]); cswap(t[3], t[7]);
+    cswap(t[3], t[5]); cswap(t[1], t[2]); cswap(t[3], t[4]); cswap(t[5], t[6]);
+    cswap(t[8], t[9]); cswap(t[10], t[11]); cswap(t[8], t[10]); cswap(t[9], t[11]); cswap(t[9], t[10]);
+    cswap(t[12], t[13]); cswap(t[14], t[15]); cswap(t[12], t[14]); cswap(t[13], t[15]); cswap(t[13], t[14]);
+    cswap(t[8], t[12]); cswap(t[10], t[14]); cswap(t[10], t[12]); cswap(t[9], t[13]); cswap(t[11], t[15]);
+    cswap(t[11], t[13]); cswap(t[9], t[10]); cswap(t[11], t[12]); cswap(t[13], t[14]);
+    cswap(t[0], t[8]); cswap(t[4], t[12]); cswap(t[4], t[8]); cswap(t[2], t[10]); cswap(t[6], t[14]);
+    cswap(t[6], t[10]); cswap(t[2], t[4]); cswap(t[6], t[8]); cswap(t[10], t[12]); cswap(t[1], t[9]);
+    cswap(t[5], t[13]); cswap(t[5], t[9]); cswap(t[3], t[11]); cswap(t[7], t[15]); cswap(t[7], t[11]);
+    cswap(t[3], t[5]); cswap(t[7], t[9]); cswap(t[11], t[13]); cswap(t[1], t[2]); cswap(t[3], t[4]);
+    cswap(t[5], t[6]); cswap(t[7], t[8]); cswap(t[9], t[10]); cswap(t[11], t[12]); cswap(t[13], t[14]);
 }
 
-// --------------------------------------------------------------------------- K2 scan
-
-__global__ void __launch_bounds__(1024) k_scan(Params P)
-{
-    __shared__ uint32_t s_a[32], s_b[32];
-    const int T = P.T;
-    const int per = (T + blockDim.x - 1) / blockDim.x;
-    const int b = threadIdx.x * per, e = min(T, b + per);
-    uint32_t sa = 0, sb = 0;
-    for (int t = b; t < e; ++t) {
-        const uint32_t c = P.tile_cnt[t];
-        sa += c;
-        sb += min(4u * c, (uint32_t)(kTilePix * kCap));
-    }
-    // block exclusive scan of (sa, sb)
-    const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
-    uint32_t xa = sa, xb = sb;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t ya = __shfl_up_sync(0xffffffffu, xa, o), yb = __shfl_up_sync(0xffffffffu, xb, o);
-        if (lane >= (unsigned)o) { xa += ya; xb += yb; }
-    }
-    if (lane == 31) { s_a[warp] = xa; s_b[warp] = xb; }
-    __syncthreads();
-    if (warp == 0) {
-        uint32_t wa = s_a[lane], wb = s_b[lane];
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t ya = __shfl_up_sync(0xffffffffu, wa, o), yb = __shfl_up_sync(0xffffffffu, wb, o);
-            if (lane >= (unsigned)o) { wa += ya; wb += yb; }
-        }
-        s_a[lane] = wa; s_b[lane] = wb;            // inclusive warp totals
-    }
-    __syncthreads();
-    uint32_t pa = (warp ? s_a[warp - 1] : 0u) + xa - sa;
-    uint32_t pb = (warp ? s_b[warp - 1] : 0u) + xb - sb;
-    for (int t = b; t < e; ++t) {
-        const uint32_t c = P.tile_cnt[t];
-        P.tile_off[t] = pa;
-        P.tile_cur[t] = pa;
-        P.tile_kbase[t] = pb;
-        pa += c;
-        pb += min(4u * c, (uint32_t)(kTilePix * kCap));
-    }
-    if (threadIdx.x == blockDim.x - 1) {
-        P.tile_off[T] = pa;
-        P.tile_kbase[T] = pb;
-        P.stats[S_PAIRS] = pa;
-    }
-}
-
-// --------------------------------------------------------------------------- K3 bin
-
-__global__ void __launch_bounds__(256) k_bin(Params P)
-{
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    int tiles[8];
-    int np = 0;
-    if (i < P.n) {
-        const float4 r = reinterpret_cast<const float4*>(P.rec + (size_t)i * P.RS)[0];
-        if (r.z >= 0.f) np = enumerate_pairs(P, r.x, r.y, r.z, tiles, nullptr);
-    }
-    const unsigned lane = lane_id();
-    const int wmax = __reduce_max_sync(0xffffffffu, np);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        if (k >= wmax) break;
-        const int t = k < np ? tiles[k] : -1;
-        const unsigned peers = __match_any_sync(0xffffffffu, t);
-        if (t >= 0) {
-            const int leader = __ffs(peers) - 1;
-            uint32_t base = 0;
-            if (lane == (unsigned)leader) base = atomicAdd(&P.tile_cur[t], (uint32_t)__popc(peers));
-            base = __shfl_sync(peers, base, leader);
-            P.bins[base + __popc(peers & lanemask_lt())] = (uint32_t)i;
-        }
-    }
-}
-
-// --------------------------------------------------------------------------- K4 raster
-
-// Sorting network (bitonic, ascending) over 16 u64 keys held in registers.
-__device__ __forceinline__ void sort16(uint64_t (&t)[16])
+// r (sorted asc, 16) <- the 16 smallest of r U t, t sorted asc in t[0..N) (N = 8 or 16):
+// bitonic split (min against reversed t) + bitonic clean.
+template <int N>
+__device__ __forceinline__ void merge_keep16(uint64_t (&r)[16], const uint64_t (&t)[16])
 {
 #pragma unroll
-    for (int k = 2; k <= 16; k <<= 1)
-#pragma unroll
-        for (int j = k >> 1; j > 0; j >>= 1)
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                const int l = i ^ j;
-                if (l > i) {
-                    if ((i & k) == 0) cswap(t[i], t[l]);
-                    else cswap(t[l], t[i]);
-                }
-            }
-}
-
-// r (sorted asc) <- the 16 smallest of r U t (both sorted asc): bitonic split + clean.
-__device__ __forceinline__ void merge16(uint64_t (&r)[16], const uint64_t (&t)[16])
-{
-#pragma unroll
-    for (int j = 0; j < 16; ++j) r[j] = r[j] < t[15 - j] ? r[j] : t[15 - j];
+    for (int j = 16 - N; j < 16; ++j) r[j] = r[j] < t[15 - j] ? r[j] : t[15 - j];
 #pragma unroll
     for (int d = 8; d > 0; d >>= 1)
 #pragma unroll
         for (int i = 0; i < 16; ++i)
             if ((i & d) == 0) cswap(r[i], r[i + d]);
 }
+
+// --------------------------------------------------------------------------- fragment weights
 
 // gamma of point record r0 = (x, y, s, alpha) at pixel (px, py) of layer l (Eq. 3):
 // beta = wx wy with wx = 1 - |x_l - px|, iota from Eq. (4) for layer l.
@@ -274,6 +119,8 @@ __device__ __forceinline__ TileCoord tile_coord(const Params& P, int t)
     return c;
 }
 
+// --------------------------------------------------------------------------- K4 raster
+
 template <int FC>
 __global__ void __launch_bounds__(kTilePix, 2) k_raster(Params P, float* __restrict__ pyramid, int save)
 {
@@ -301,7 +148,7 @@ __global__ void __launch_bounds__(kTilePix, 2) k_raster(Params P, float* __restr
         const int m = (int)min((uint32_t)kChunk, b1 - c0);
         s_cnt[tid] = 0;
         __syncthreads();
-        // phase A: stage this chunk's points, compute their fragments in this tile
+        // phase A: this chunk's pairs -> fragments of this tile (footprint origin in the bin)
         uint64_t fk[kPairsPerThread][4];
         uint32_t fq[kPairsPerThread][4];             // (q | rank << 8), 0xffffffff = none
 #pragma unroll
@@ -310,22 +157,17 @@ __global__ void __launch_bounds__(kTilePix, 2) k_raster(Params P, float* __restr
             for (int c = 0; c < 4; ++c) fq[k][c] = 0xffffffffu;
             const int j = tid + k * kTilePix;
             if (j < m) {
-                const uint32_t i = P.bins[c0 + j];
-                const float4 r0 = reinterpret_cast<const float4*>(P.rec + (size_t)i * P.RS)[0];
-                const float z = P.zbuf[i];
-                const uint64_t key = ((uint64_t)__float_as_uint(z) << 32) | i;
-                Foot f;
-                if (footprint(r0.x, r0.y, tc.l, G.W, G.H, f)) {
+                const uint64_t key = P.bin_key[c0 + j];
+                const uint32_t o = P.bin_orig[c0 + j];
+                const int qx0 = (int)(o & 31u) - 1, qy0 = (int)(o >> 5) - 1;
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) {
-                        const int qx = f.x0 + (c & 1), qy = f.y0 + (c >> 1);
-                        if (qx >= x_lo && qx < x_lo + kTile && qx < G.W && qy >= y_lo && qy < y_lo + kTile &&
-                            qy < G.H) {
-                            const uint32_t q = (uint32_t)((qy - y_lo) * kTile + (qx - x_lo));
-                            const uint32_t rank = atomicAdd(&s_cnt[q], 1u);
-                            fk[k][c] = key;
-                            fq[k][c] = q | (rank << 8);
-                        }
+                for (int c = 0; c < 4; ++c) {
+                    const int qx = qx0 + (c & 1), qy = qy0 + (c >> 1);
+                    if (qx >= 0 && qx < kTile && qy >= 0 && qy < kTile && x_lo + qx < G.W && y_lo + qy < G.H) {
+                        const uint32_t q = (uint32_t)(qy * kTile + qx);
+                        const uint32_t rank = atomicAdd(&s_cnt[q], 1u);
+                        fk[k][c] = key;
+                        fq[k][c] = q | (rank << 8);
                     }
                 }
             }
@@ -333,7 +175,7 @@ __global__ void __launch_bounds__(kTilePix, 2) k_raster(Params P, float* __restr
         __syncthreads();
         uint32_t chunk_total;
         const uint32_t my_cnt = s_cnt[tid];
-        const uint32_t my_base = block_excl_scan256(my_cnt, s_warp, &chunk_total);
+        const uint32_t my_base = block_excl_scan(my_cnt, s_warp, &chunk_total);
         s_base[tid] = my_base;
         __syncthreads();
         // phase B: counting-sort scatter by pixel
@@ -343,42 +185,80 @@ __global__ void __launch_bounds__(kTilePix, 2) k_raster(Params P, float* __restr
             for (int c = 0; c < 4; ++c)
                 if (fq[k][c] != 0xffffffffu) s_keys[s_base[fq[k][c] & 0xffu] + (fq[k][c] >> 8)] = fk[k][c];
         __syncthreads();
-        // phase C: merge this pixel's new fragments into its running top-16
-        for (uint32_t g = 0; g < my_cnt; g += 16) {
+        // phase C: merge this pixel's new fragments into its running top-16.  Network sizes are
+        // chosen per warp (8 when no lane of the warp has more than 8 keys left in the group).
+        const uint32_t wcnt = __reduce_max_sync(0xffffffffu, my_cnt);
+        for (uint32_t g = 0; g < wcnt; g += 16) {
+            const uint32_t rem = my_cnt > g ? my_cnt - g : 0u;
+            const bool first = __all_sync(0xffffffffu, total == 0 && g == 0);
             uint64_t tk[16];
+            if (__reduce_max_sync(0xffffffffu, rem) <= 8u) {
 #pragma unroll
-            for (int j = 0; j < 16; ++j) tk[j] = (g + j < my_cnt) ? s_keys[my_base + g + j] : kKeyMax;
-            sort16(tk);
-            merge16(r, tk);
+                for (int j = 0; j < 16; ++j) tk[j] = (j < 8 && (uint32_t)j < rem) ? s_keys[my_base + g + j] : kKeyMax;
+                sort_small<8>(tk);
+                if (first) {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) r[j] = tk[j];
+                } else {
+                    merge_keep16<8>(r, tk);
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) tk[j] = ((uint32_t)j < rem) ? s_keys[my_base + g + j] : kKeyMax;
+                sort_small<16>(tk);
+                if (first) {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) r[j] = tk[j];
+                } else {
+                    merge_keep16<16>(r, tk);
+                }
+            }
         }
         total += my_cnt;
         __syncthreads();
     }
 
-    // phase D: front-to-back blend of the kept list (Eqs. 5-6; alpha_m := gamma_m, Q10)
+    // phase D: front-to-back blend of the kept list (Eqs. 5-6; alpha_m := gamma_m, Q10).
+    // Record gathers are issued kBatch at a time.  Without a following backward the loop
+    // stops once T == 0 exactly (later terms vanish); with one, every gamma_m is needed.
     const int K = valid ? (int)min(total, (uint32_t)kCap) : 0;
+    uint32_t ktot;
+    const uint32_t koff = block_excl_scan((uint32_t)K, s_warp, &ktot);
+    const size_t kidx = (size_t)P.tile_kbase[t] + koff;
     float C[FC];
 #pragma unroll
     for (int c = 0; c < FC; ++c) C[c] = 0.f;
     float A = 0.f, T = 1.f;
 #pragma unroll
-    for (int mm = 0; mm < kCap; ++mm) {
-        if (mm < K && T > 0.f) {                        // T == 0 exactly: later terms vanish
-            const uint32_t i = (uint32_t)r[mm];
-            const float4* rp = reinterpret_cast<const float4*>(P.rec + (size_t)i * P.RS);
-            const float4 r0 = rp[0];
-            const FragW w = frag_weights(r0, tc.l, P.n_layers, px, py);
-            const float tg = T * w.gamma;
+    for (int b = 0; b < kCap / kBatch; ++b) {
+        if (b * kBatch >= K || (!save && T == 0.f)) break;
+        float4 rb[kBatch][1 + FC / 4];
 #pragma unroll
-            for (int c4 = 0; c4 < FC / 4; ++c4) {
-                const float4 tau = rp[1 + c4];
-                C[4 * c4 + 0] = fmaf(tg, tau.x, C[4 * c4 + 0]);
-                C[4 * c4 + 1] = fmaf(tg, tau.y, C[4 * c4 + 1]);
-                C[4 * c4 + 2] = fmaf(tg, tau.z, C[4 * c4 + 2]);
-                C[4 * c4 + 3] = fmaf(tg, tau.w, C[4 * c4 + 3]);
+        for (int u = 0; u < kBatch; ++u) {
+            const int mm = b * kBatch + u;                       // compile-time register index
+            const uint32_t ii = (uint32_t)(mm < K ? r[mm] : r[0]);
+            const float4* rp = reinterpret_cast<const float4*>(P.rec + (size_t)ii * P.RS);
+#pragma unroll
+            for (int c4 = 0; c4 <= FC / 4; ++c4) rb[u][c4] = __ldg(rp + c4);
+        }
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) {
+            const int mm = b * kBatch + u;
+            if (mm < K) {
+                const FragW w = frag_weights(rb[u][0], tc.l, P.n_layers, px, py);
+                const float tg = T * w.gamma;
+#pragma unroll
+                for (int c4 = 0; c4 < FC / 4; ++c4) {
+                    const float4 tau = rb[u][1 + c4];
+                    C[4 * c4 + 0] = fmaf(tg, tau.x, C[4 * c4 + 0]);
+                    C[4 * c4 + 1] = fmaf(tg, tau.y, C[4 * c4 + 1]);
+                    C[4 * c4 + 2] = fmaf(tg, tau.z, C[4 * c4 + 2]);
+                    C[4 * c4 + 3] = fmaf(tg, tau.w, C[4 * c4 + 3]);
+                }
+                A += tg;
+                T = T * (1.0f - w.gamma);
+                if (save) P.kept_gamma[kidx + mm] = w.gamma;
             }
-            A += tg;
-            T = T * (1.0f - w.gamma);
         }
     }
     if (valid) {
@@ -391,27 +271,14 @@ __global__ void __launch_bounds__(kTilePix, 2) k_raster(Params P, float* __restr
     }
 
     // phase E: store the sorted kept lists and per-pixel metadata
-    uint32_t ktot;
-    const uint32_t koff = block_excl_scan256((uint32_t)K, s_warp, &ktot);
     P.pix_cnt[(size_t)t * kTilePix + tid] = valid ? total : 0u;
     P.pix_meta[(size_t)t * kTilePix + tid] = (koff << 5) | (uint32_t)K;
     if (save) {
-        uint64_t* kp = P.kept + P.tile_kbase[t] + koff;
+        uint64_t* kp = P.kept + kidx;
 #pragma unroll
         for (int mm = 0; mm < kCap; ++mm)
             if (mm < K) kp[mm] = r[mm];
     }
-    // statistics (n_frag, n_kept, n_trunc, max_list)
-    const uint32_t vt = valid ? total : 0u;
-    const uint32_t wf = __reduce_add_sync(0xffffffffu, vt);
-    const uint32_t wtr = __popc(__ballot_sync(0xffffffffu, vt > (uint32_t)kCap));
-    const uint32_t wmx = __reduce_max_sync(0xffffffffu, vt);
-    if (lane_id() == 0) {
-        if (wf) atomicAdd(&P.stats[S_FRAG], (unsigned long long)wf);
-        if (wtr) atomicAdd(&P.stats[S_TRUNC], (unsigned long long)wtr);
-        if (wmx) atomicMax(&P.stats[S_MAXLIST], (unsigned long long)wmx);
-    }
-    if (tid == 0 && ktot) atomicAdd(&P.stats[S_KEPT], (unsigned long long)ktot);
 }
 
 // --------------------------------------------------------------------------- K5 backward
@@ -428,32 +295,30 @@ __global__ void __launch_bounds__(kTilePix) k_backward(Params P, const float* __
     const uint32_t meta = P.pix_meta[(size_t)t * kTilePix + tid];
     const int K = (int)(meta & 31u);
     if (K == 0) return;
-    const uint64_t* kp = P.kept + P.tile_kbase[t] + (meta >> 5);
+    const size_t kidx = (size_t)P.tile_kbase[t] + (meta >> 5);
+    const uint64_t* kp = P.kept + kidx;
+    const float* gm = P.kept_gamma + kidx;
 
     // upstream gradient of this pixel: gC (F channels) and gA
     const int64_t plane = (int64_t)G.W * G.H;
     const float* gp = gpyr + G.float_off + (int64_t)py * G.W + px;
     float gC[FC];
 #pragma unroll
-    for (int c = 0; c < FC; ++c) gC[c] = (c < P.F) ? gp[c * plane] : 0.f;
-    const float gA = gp[P.F * plane];
+    for (int c = 0; c < FC; ++c) gC[c] = (c < P.F) ? __ldg(gp + c * plane) : 0.f;
+    const float gA = __ldg(gp + P.F * plane);
 
-    // forward replay: gamma_m and T_m (Eq. 6)
+    // T_m from the saved gamma_m (Eq. 6) -- no record gathers
     float gam[kCap], Tm[kCap];
     float T = 1.f;
 #pragma unroll
     for (int mm = 0; mm < kCap; ++mm) {
-        gam[mm] = 0.f; Tm[mm] = 0.f;
-        if (mm < K) {
-            const uint32_t i = (uint32_t)kp[mm];
-            const float4 r0 = reinterpret_cast<const float4*>(P.rec + (size_t)i * P.RS)[0];
-            const FragW w = frag_weights(r0, tc.l, P.n_layers, px, py);
-            gam[mm] = w.gamma;
-            Tm[mm] = T;
-            T = T * (1.0f - w.gamma);
-        }
+        gam[mm] = mm < K ? __ldg(gm + mm) : 0.f;
+        Tm[mm] = T;
+        T = T * (1.0f - gam[mm]);
     }
-    // reverse replay with suffix recurrences (division-free)
+    // reverse replay with suffix recurrences (division-free):
+    //   dL/dgamma_m = T_m (<gC, tau_m - B_m> + gA (1 - b_m)),
+    //   B_{m-1} = gamma_m tau_m + (1 - gamma_m) B_m,   b_{m-1} = gamma_m + (1 - gamma_m) b_m
     float B[FC];
 #pragma unroll
     for (int c = 0; c < FC; ++c) B[c] = 0.f;
@@ -461,22 +326,33 @@ __global__ void __launch_bounds__(kTilePix) k_backward(Params P, const float* __
     const float sc = pow2_neg(tc.l);
     const Cam& cam = P.cam;
 #pragma unroll
-    for (int mm = kCap - 1; mm >= 0; --mm) {
-        if (mm < K) {
-            const uint64_t key = kp[mm];
-            const uint32_t i = (uint32_t)key;
-            const float z = __uint_as_float((uint32_t)(key >> 32));
-            const float4* rp = reinterpret_cast<const float4*>(P.rec + (size_t)i * P.RS);
-            const float4 r0 = rp[0];
+    for (int b = kCap / kBatch - 1; b >= 0; --b) {
+        if (b * kBatch >= K) continue;
+        float4 rb[kBatch][1 + FC / 4];
+        uint64_t kb[kBatch];
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) {
+            const int mm = min(b * kBatch + u, K - 1);
+            kb[u] = __ldg(reinterpret_cast<const unsigned long long*>(kp) + mm);
+            const float4* rp = reinterpret_cast<const float4*>(P.rec + (size_t)(uint32_t)kb[u] * P.RS);
+#pragma unroll
+            for (int c4 = 0; c4 <= FC / 4; ++c4) rb[u][c4] = __ldg(rp + c4);
+        }
+#pragma unroll
+        for (int u = kBatch - 1; u >= 0; --u) {
+            const int mm = b * kBatch + u;
+            if (mm >= K) continue;
+            const uint32_t i = (uint32_t)kb[u];
+            const float z = __uint_as_float((uint32_t)(kb[u] >> 32));
+            const float4 r0 = rb[u][0];
             const FragW w = frag_weights(r0, tc.l, P.n_layers, px, py);
             const float g = gam[mm], tm = Tm[mm];
             float tau[FC];
 #pragma unroll
             for (int c4 = 0; c4 < FC / 4; ++c4) {
-                const float4 v = rp[1 + c4];
-                tau[4 * c4 + 0] = v.x; tau[4 * c4 + 1] = v.y; tau[4 * c4 + 2] = v.z; tau[4 * c4 + 3] = v.w;
+                tau[4 * c4 + 0] = rb[u][1 + c4].x; tau[4 * c4 + 1] = rb[u][1 + c4].y;
+                tau[4 * c4 + 2] = rb[u][1 + c4].z; tau[4 * c4 + 3] = rb[u][1 + c4].w;
             }
-            // d out / d gamma_m = T_m (<gC, tau_m - B_m> + gA (1 - b_m))
             float dg = gA * (1.0f - bb);
 #pragma unroll
             for (int c = 0; c < FC; ++c) dg = fmaf(gC[c], tau[c] - B[c], dg);
@@ -498,7 +374,6 @@ __global__ void __launch_bounds__(kTilePix) k_backward(Params P, const float* __
             const float gsw = gs * cam.f * iz;
             float* grow = grad + (size_t)i * P.G;
             red_add_v4(grow, gX, gY, gZ, gsw);
-            // (alpha, tau[0..FC-1]) in 16-B chunks
             float v[FC + 4];
             v[0] = galpha;
 #pragma unroll
@@ -507,7 +382,6 @@ __global__ void __launch_bounds__(kTilePix) k_backward(Params P, const float* __
 #pragma unroll
             for (int c4 = 0; c4 < (FC + 4) / 4; ++c4)
                 if (4 * c4 < P.F + 1) red_add_v4(grow + 4 + 4 * c4, v[4 * c4], v[4 * c4 + 1], v[4 * c4 + 2], v[4 * c4 + 3]);
-            // suffix recurrences
 #pragma unroll
             for (int c = 0; c < FC; ++c) B[c] = g * tau[c] + (1.0f - g) * B[c];
             bb = g + (1.0f - g) * bb;

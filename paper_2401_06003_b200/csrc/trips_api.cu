@@ -2,6 +2,7 @@
 //
 // Validation, plan/workspace layout, launch sequencing and optional per-stage CUDA-event
 // timing.  No device allocation, no host synchronisation on the hot path.
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdio>
@@ -18,7 +19,7 @@ namespace {
 std::atomic<long long> g_launches{0};
 thread_local char g_msg[256];
 
-constexpr int kStages = 5;   // 0 project, 1 scan, 2 bin, 3 raster, 4 backward
+constexpr int kStages = 5;   // 0 count, 1 emit, 2 sort, 3 raster, 4 backward (kernel groups)
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -34,7 +35,8 @@ struct trips_plan {
     LayerGeom L[kMaxLayers];
     uint64_t kcap;
     // workspace layout (byte offsets)
-    size_t off_rec, off_z, off_tcnt, off_toff, off_tcur, off_tkb, off_bins, off_pcnt, off_pmeta, off_kept,
+    int32_t ctas;           // binning CTAs (persistent grid)
+    size_t off_rec, off_hist, off_cvis, off_toff, off_tkb, off_bkey, off_borig, off_pcnt, off_pmeta, off_kept, off_kgam,
         off_stats, ws_bytes;
     // state
     const void* ws_bound = nullptr;
@@ -76,7 +78,6 @@ struct StageScope {
             cudaEventRecord(ev.a, st);
         }
         p->launches[s]++;
-        g_launches++;
     }
     ~StageScope()
     {
@@ -94,7 +95,44 @@ int cuda_status(cudaError_t e)
     return TRIPS_ERR_CUDA;
 }
 
-int check_launch() { return cuda_status(cudaGetLastError()); }
+int num_sms()
+{
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0)
+            sms = 148;                        // B200; plan creation must work without a GPU
+        cudaGetLastError();
+    }
+    return sms;
+}
+
+template <int FC>
+int set_emit_attr(size_t bytes)
+{
+    return (int)cudaFuncSetAttribute(k_emit<FC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+// Opt the binning kernels into > 48 KB of dynamic shared memory (one counter per tile).
+int set_smem_attrs(size_t bytes)
+{
+    static size_t done = 0;
+    if (bytes <= done) return TRIPS_OK;
+    cudaError_t e = cudaFuncSetAttribute(k_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    int bad = (int)e;
+    bad |= set_emit_attr<4>(bytes) | set_emit_attr<8>(bytes) | set_emit_attr<12>(bytes) | set_emit_attr<16>(bytes) |
+           set_emit_attr<20>(bytes) | set_emit_attr<24>(bytes) | set_emit_attr<28>(bytes) | set_emit_attr<32>(bytes);
+    if (bad) return cuda_status(cudaGetLastError());
+    done = bytes;
+    return TRIPS_OK;
+}
+
+int check_launch()
+{
+    g_launches++;
+    return cuda_status(cudaGetLastError());
+}
 
 Params make_params(const trips_plan* p, void* ws)
 {
@@ -107,15 +145,16 @@ Params make_params(const trips_plan* p, void* ws)
     P.cam = p->cam;
     char* b = static_cast<char*>(ws);
     P.rec = reinterpret_cast<float*>(b + p->off_rec);
-    P.zbuf = reinterpret_cast<float*>(b + p->off_z);
-    P.tile_cnt = reinterpret_cast<uint32_t*>(b + p->off_tcnt);
+    P.hist = reinterpret_cast<uint32_t*>(b + p->off_hist);
+    P.cta_vis = reinterpret_cast<uint32_t*>(b + p->off_cvis);
     P.tile_off = reinterpret_cast<uint32_t*>(b + p->off_toff);
-    P.tile_cur = reinterpret_cast<uint32_t*>(b + p->off_tcur);
     P.tile_kbase = reinterpret_cast<uint32_t*>(b + p->off_tkb);
-    P.bins = reinterpret_cast<uint32_t*>(b + p->off_bins);
+    P.bin_key = reinterpret_cast<uint64_t*>(b + p->off_bkey);
+    P.bin_orig = reinterpret_cast<uint16_t*>(b + p->off_borig);
     P.pix_cnt = reinterpret_cast<uint32_t*>(b + p->off_pcnt);
     P.pix_meta = reinterpret_cast<uint32_t*>(b + p->off_pmeta);
     P.kept = reinterpret_cast<uint64_t*>(b + p->off_kept);
+    P.kept_gamma = reinterpret_cast<float*>(b + p->off_kgam);
     P.stats = reinterpret_cast<unsigned long long*>(b + p->off_stats);
     return P;
 }
@@ -171,19 +210,21 @@ int trips_plan_create(const trips_config* cfg, int32_t width, int32_t height, in
     p->pyr_floats = pix * (F + 1);
     const uint64_t kc1 = (uint64_t)tiles * kTilePix * kCap, kc2 = (uint64_t)max_points * 32;
     p->kcap = kc1 < kc2 ? kc1 : kc2;
-    if (p->kcap >= (uint64_t(1) << 32)) { delete p; return TRIPS_ERR_ARG; }
+    if (p->kcap >= (uint64_t(1) << 32) || tiles > kMaxTilesSmem) { delete p; return TRIPS_ERR_ARG; }
     const size_t N = (size_t)(max_points > 0 ? max_points : 1);
     size_t o = 0;
-    p->off_rec = o;   o = align256(o + N * p->RS * sizeof(float));
-    p->off_z = o;     o = align256(o + N * sizeof(float));
-    p->off_tcnt = o;  o = align256(o + (size_t)tiles * 4);
-    p->off_toff = o;  o = align256(o + ((size_t)tiles + 1) * 4);
-    p->off_tcur = o;  o = align256(o + (size_t)tiles * 4);
-    p->off_tkb = o;   o = align256(o + ((size_t)tiles + 1) * 4);
-    p->off_bins = o;  o = align256(o + 8 * N * 4);
+    p->ctas = num_sms() * kBinCtasPerSm;
+    p->off_rec = o;    o = align256(o + N * p->RS * sizeof(float));
+    p->off_hist = o;   o = align256(o + (size_t)p->ctas * tiles * 4);
+    p->off_cvis = o;   o = align256(o + (size_t)p->ctas * 4);
+    p->off_toff = o;   o = align256(o + ((size_t)tiles + 1) * 4);
+    p->off_tkb = o;    o = align256(o + ((size_t)tiles + 1) * 4);
+    p->off_bkey = o;   o = align256(o + 8 * N * 8);
+    p->off_borig = o;  o = align256(o + 8 * N * 2);
     p->off_pcnt = o;  o = align256(o + (size_t)tiles * kTilePix * 4);
     p->off_pmeta = o; o = align256(o + (size_t)tiles * kTilePix * 4);
     p->off_kept = o;  o = align256(o + (p->kcap ? p->kcap : 1) * 8);
+    p->off_kgam = o;  o = align256(o + (p->kcap ? p->kcap : 1) * 4);
     p->off_stats = o; o = align256(o + S_COUNT * 8);
     p->ws_bytes = o;
     *out = p;
@@ -238,16 +279,23 @@ int trips_project(trips_plan* p, void* ws, const trips_camera* c, int64_t n, con
     cam.near_plane = c->near_plane;
     Params P = make_params(p, ws);
     P.pos = pos; P.sw = world_size; P.alpha = opacity; P.desc = desc;
-    int rc = cuda_status(cudaMemsetAsync(P.tile_cnt, 0, (size_t)p->T * 4, st));
+    int rc = cuda_status(cudaMemsetAsync(P.stats, 0, S_COUNT * 8, st));
     if (rc) return rc;
-    rc = cuda_status(cudaMemsetAsync(P.stats, 0, S_COUNT * 8, st));
+    rc = cuda_status(cudaMemsetAsync(P.tile_off, 0, ((size_t)p->T + 1) * 4, st));
     if (rc) return rc;
-    if (n > 0) {
+    const size_t hsm = (size_t)p->T * 4;
+    if ((rc = set_smem_attrs(hsm))) return rc;
+    {
         StageScope sc(p, 0, st);
-        const int blocks = (int)((n + 255) / 256);
-        TRIPS_FC_SWITCH(p->FC, (k_project<kFC><<<blocks, 256, 0, st>>>(P, level_out, proj_out)));
-        rc = check_launch();
-        if (rc) return rc;
+        k_count<<<p->ctas, kBinThreads, hsm, st>>>(P);
+        if ((rc = check_launch())) return rc;
+        k_tscan<<<1, 1024, 0, st>>>(P);
+        if ((rc = check_launch())) return rc;
+    }
+    {
+        StageScope sc(p, 1, st);
+        TRIPS_FC_SWITCH(p->FC, (k_emit<kFC><<<p->ctas, kBinThreads, hsm, st>>>(P, level_out, proj_out)));
+        if ((rc = check_launch())) return rc;
     }
     p->stage = 1;
     return TRIPS_OK;
@@ -261,16 +309,6 @@ int trips_splat_forward(trips_plan* p, void* ws, float* pyramid, uint32_t flags,
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     Params P = make_params(p, ws);
     int rc;
-    {
-        StageScope sc(p, 1, st);
-        k_scan<<<1, 1024, 0, st>>>(P);
-        if ((rc = check_launch())) return rc;
-    }
-    if (p->n > 0) {
-        StageScope sc(p, 2, st);
-        k_bin<<<(int)((p->n + 255) / 256), 256, 0, st>>>(P);
-        if ((rc = check_launch())) return rc;
-    }
     {
         StageScope sc(p, 3, st);
         const int save = (flags & TRIPS_FWD_SAVE_FOR_BACKWARD) ? 1 : 0;
@@ -302,14 +340,22 @@ int trips_read_stats(const trips_plan* p, const void* ws, trips_stats* out, void
     if (!p || !ws || !out) return TRIPS_ERR_ARG;
     if (p->stage == 0 || ws != p->ws_bound) return TRIPS_ERR_STATE;
     unsigned long long h[S_COUNT];
+    uint32_t npairs = 0;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    int rc = cuda_status(cudaMemcpyAsync(h, static_cast<const char*>(ws) + p->off_stats, sizeof(h),
-                                         cudaMemcpyDeviceToHost, st));
+    Params P = make_params(p, const_cast<void*>(ws));
+    int rc = cuda_status(cudaMemsetAsync(P.stats, 0, S_COUNT * 8, st));
+    if (rc) return rc;
+    const int npix = p->stage >= 2 ? p->T * kTilePix : 0;
+    k_stats<<<std::max(1, std::min(148 * 4, (npix + 255) / 256)), 256, 0, st>>>(P, p->ctas, npix);
+    if ((rc = check_launch())) return rc;
+    rc = cuda_status(cudaMemcpyAsync(h, P.stats, sizeof(h), cudaMemcpyDeviceToHost, st));
+    if (rc) return rc;
+    rc = cuda_status(cudaMemcpyAsync(&npairs, P.tile_off + p->T, 4, cudaMemcpyDeviceToHost, st));
     if (rc) return rc;
     if ((rc = cuda_status(cudaStreamSynchronize(st)))) return rc;
-    out->n_culled = (int64_t)h[S_CULLED];
     out->n_visible = (int64_t)h[S_VISIBLE];
-    out->n_pairs = (int64_t)h[S_PAIRS];
+    out->n_culled = p->n - out->n_visible;
+    out->n_pairs = (int64_t)npairs;
     out->n_frag = (int64_t)h[S_FRAG];
     out->n_kept = (int64_t)h[S_KEPT];
     out->n_trunc_pixels = (int64_t)h[S_TRUNC];
@@ -325,7 +371,6 @@ int trips_debug_export(const trips_plan* p, const void* ws, int32_t what, void* 
     if (what == TRIPS_EXPORT_KEPT && p->stage != 2) return TRIPS_ERR_STATE;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     Params P = make_params(p, const_cast<void*>(ws));
-    g_launches++;
     k_export<<<p->T, kTilePix, 0, st>>>(P, what, dst);
     int rc = check_launch();
     if (rc) return rc;
