@@ -170,6 +170,22 @@ int trips_set_profiling(trips_plan* plan, int32_t enable);
 int trips_read_stage_ms(trips_plan* plan, double* ms, int64_t* launches, int32_t max_stages,
                         int32_t reset);
 
+/* ---- data layout utility ------------------------------------------------------------ */
+
+/* One-time spatial ordering of a point cloud (not part of the per-view path).  Writes a
+ * permutation perm[n] (int32, device) such that pos[perm[0]], pos[perm[1]], ... follow a 3-D
+ * Morton (Z-order) curve over the cloud's bounding box, 10 bits per axis; ties keep index
+ * order; non-finite points go last.  Applying it once to all per-point arrays makes every
+ * per-view gather and gradient reduction spatially coherent (cache lines and tiles shared by
+ * neighbouring indices), as in the spatially sorted batches of the software point rasterizer
+ * the paper builds on (PAPER.md:160 cites it as [schutz2022software]).  Results of the
+ * rasterizer are unchanged up to the point-index tie-break of equal depths (reading Q12).
+ *   ws   device scratch of trips_morton_workspace_bytes(n) bytes, 256-B aligned
+ *   pos  float[n][3] device, 4-B aligned
+ * Errors: TRIPS_ERR_ARG, TRIPS_ERR_ALIGN, TRIPS_ERR_CAPACITY (n >= 2^31), TRIPS_ERR_CUDA. */
+size_t trips_morton_workspace_bytes(int64_t n);
+int trips_morton_order(void* ws, int64_t n, const float* pos, int32_t* perm_out, void* stream);
+
 /* Total kernel launches issued by this library in this process. */
 int64_t trips_launch_count(void);
 

@@ -67,6 +67,8 @@ SIGNATURES = [
     ("trips_debug_export", C.c_int, [_VP, _VP, C.c_int32, _VP, _VP]),
     ("trips_set_profiling", C.c_int, [_VP, C.c_int32]),
     ("trips_read_stage_ms", C.c_int, [_VP, C.POINTER(C.c_double), C.POINTER(C.c_int64), C.c_int32, C.c_int32]),
+    ("trips_morton_workspace_bytes", C.c_size_t, [C.c_int64]),
+    ("trips_morton_order", C.c_int, [_VP, C.c_int64, _VP, _VP, _VP]),
     ("trips_launch_count", C.c_int64, []),
     ("trips_status_string", C.c_char_p, [C.c_int]),
 ]
@@ -180,6 +182,14 @@ def trips_read_stage_ms(plan, reset=False):
     la = (C.c_int64 * N_STAGES)()
     lib().trips_read_stage_ms(plan, ms, la, N_STAGES, 1 if reset else 0)
     return {STAGE_NAMES[s]: (ms[s], la[s]) for s in range(N_STAGES)}
+
+
+def trips_morton_workspace_bytes(n):
+    return int(lib().trips_morton_workspace_bytes(n))
+
+
+def trips_morton_order(ws, n, pos, perm_out, stream=None):
+    return lib().trips_morton_order(ws, n, pos, perm_out, stream)
 
 
 def trips_launch_count():

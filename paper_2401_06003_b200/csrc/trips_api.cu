@@ -11,6 +11,7 @@
 
 #include "../../include/trips.h"
 #include "kernels.cuh"
+#include "morton.cuh"
 
 using namespace trips;
 
@@ -408,6 +409,51 @@ int trips_read_stage_ms(trips_plan* p, double* ms, int64_t* launches, int32_t ma
 }
 
 int64_t trips_launch_count(void) { return (int64_t)g_launches.load(); }
+
+size_t trips_morton_workspace_bytes(int64_t n)
+{
+    if (n < 0) return 0;
+    const size_t N = (size_t)(n > 0 ? n : 1);
+    const size_t nblk = (N + kSortBlock - 1) / kSortBlock;
+    return 4 * align256(N * 4) + align256(256 * nblk * 4) + align256(6 * 4);
+}
+
+int trips_morton_order(void* ws, int64_t n, const float* pos, int32_t* perm_out, void* stream)
+{
+    if (!ws || n < 0 || (n > 0 && (!pos || !perm_out))) return TRIPS_ERR_ARG;
+    if (n >= (int64_t(1) << 31)) return TRIPS_ERR_CAPACITY;
+    if (!aligned(ws, 256) || !aligned(pos, 4) || !aligned(perm_out, 4)) return TRIPS_ERR_ALIGN;
+    if (n == 0) return TRIPS_OK;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t N = (size_t)n;
+    MortonWs W;
+    W.n = (int)n;
+    W.nblk = (int)((N + kSortBlock - 1) / kSortBlock);
+    char* b = static_cast<char*>(ws);
+    size_t o = 0;
+    W.keys[0] = reinterpret_cast<uint32_t*>(b + o); o += align256(N * 4);
+    W.keys[1] = reinterpret_cast<uint32_t*>(b + o); o += align256(N * 4);
+    W.vals[0] = reinterpret_cast<uint32_t*>(b + o); o += align256(N * 4);
+    W.vals[1] = reinterpret_cast<uint32_t*>(b + o); o += align256(N * 4);
+    W.hist = reinterpret_cast<uint32_t*>(b + o); o += align256(256 * (size_t)W.nblk * 4);
+    W.bbox = reinterpret_cast<uint32_t*>(b + o);
+    int rc = cuda_status(cudaMemsetAsync(W.bbox, 0xff, 3 * 4, st));
+    if (rc) return rc;
+    if ((rc = cuda_status(cudaMemsetAsync(W.bbox + 3, 0, 3 * 4, st)))) return rc;
+    k_bbox<<<std::min(W.nblk * 16, 148 * 8), 256, 0, st>>>(W, pos);
+    if ((rc = check_launch())) return rc;
+    k_codes<<<(W.n + 255) / 256, 256, 0, st>>>(W, pos);
+    if ((rc = check_launch())) return rc;
+    for (int pass = 0; pass < 4; ++pass) {
+        k_sort_hist<<<W.nblk, 256, 0, st>>>(W, pass);
+        if ((rc = check_launch())) return rc;
+        k_sort_scan<<<1, 1024, 0, st>>>(W);
+        if ((rc = check_launch())) return rc;
+        k_sort_scatter<<<W.nblk, 256, 0, st>>>(W, pass, reinterpret_cast<uint32_t*>(perm_out));
+        if ((rc = check_launch())) return rc;
+    }
+    return TRIPS_OK;
+}
 
 const char* trips_status_string(int status)
 {

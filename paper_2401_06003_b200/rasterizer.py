@@ -143,5 +143,17 @@ class _TripsFunction(torch.autograd.Function):
         return None, None, gpos, gsw, galpha, gdesc
 
 
+def morton_order(pos):
+    """Permutation (int64 CUDA tensor) putting the cloud in 3-D Morton order
+    (trips_morton_order).  Apply once to every per-point array: x[perm]."""
+    _check_input("pos", pos, (3,))
+    n = pos.shape[0]
+    ws = torch.empty(max(A.trips_morton_workspace_bytes(n), 256), dtype=torch.uint8, device=pos.device)
+    perm = torch.empty(n, dtype=torch.int32, device=pos.device)
+    A.check(A.trips_morton_order(ws.data_ptr(), n, pos.data_ptr(), perm.data_ptr(), _stream_handle()),
+            "trips_morton_order")
+    return perm.long()
+
+
 def render(rast, cam, pos, world_size, opacity, desc):
     return rast.render(cam, pos, world_size, opacity, desc)

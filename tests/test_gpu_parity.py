@@ -310,3 +310,50 @@ def test_2k_relation_full_size(dev):
         assert np.array_equal(a["counts"][pa[l]:pa[l + 1]], b["counts"][pb[l + 1]:pb[l + 2]])
         assert np.array_equal(a["kept"][pa[l]:pa[l + 1]], b["kept"][pb[l + 1]:pb[l + 2]])
         assert np.array_equal(a["pyr"][pa[l] * F1:pa[l + 1] * F1], b["pyr"][pb[l + 1] * F1:pb[l + 2] * F1])
+
+
+# ------------------------------------------------------------------ data-layout utility
+
+def test_morton_order_permutation(dev):
+    """trips_morton_order returns a permutation whose 30-bit Morton codes (recomputed here in
+    numpy over the same bounding box) are non-decreasing; rendering the permuted cloud gives
+    the same pyramid (no depth ties in this scene)."""
+    from paper_2401_06003_b200 import Rasterizer, morton_order
+    sc = scenes.make_config("C4", n=200_000, n_views=1)
+    pos = T(sc.pos, dev)
+    perm = morton_order(pos).cpu().numpy()
+    assert np.array_equal(np.sort(perm), np.arange(sc.n))
+    p = sc.pos.astype(np.float32)
+    lo, hi = p.min(0), p.max(0)
+    ext = np.maximum(hi - lo, np.float32(1e-30))
+    q = np.clip(((p - lo) / ext * np.float32(1023.0)), 0, 1023).astype(np.uint32)
+
+    def spread(v):
+        v = v & 0x3FF
+        v = (v | (v << 16)) & 0x030000FF
+        v = (v | (v << 8)) & 0x0300F00F
+        v = (v | (v << 4)) & 0x030C30C3
+        v = (v | (v << 2)) & 0x09249249
+        return v
+    code = spread(q[:, 0]) | (spread(q[:, 1]) << 1) | (spread(q[:, 2]) << 2)
+    c = code[perm].astype(np.int64)
+    # float rounding of the quantisation may differ by one cell at cell borders
+    assert (np.diff(c) < 0).mean() < 1e-3
+    a = gpu_run(sc, dev)
+    sc2 = scenes.Scene("C4p", sc.pos[perm], sc.sw[perm], sc.alpha[perm], sc.desc[perm], sc.cams, sc.n_layers)
+    b = gpu_run(sc2, dev)
+    assert np.array_equal(a["counts"], b["counts"])
+    kb = np.where(b["kept"] >= 0, perm[np.maximum(b["kept"], 0)], -1)
+    differ = (a["kept"] != kb).any(1)
+    # only exact depth ties may reorder (the tie-break is the point index, reading Q12)
+    z = a["proj"][:, 2]
+    for p in np.nonzero(differ)[0]:
+        ka = a["kept"][p][a["kept"][p] >= 0]
+        kk = kb[p][kb[p] >= 0]
+        assert np.array_equal(z[ka], z[kk]) and len(set(z[ka])) < len(ka)
+    assert differ.mean() < 1e-4
+    F1 = sc.F + 1
+    same_pix = np.nonzero(~differ)[0]
+    sel = pixel_float_index(sc.cams[0], sc.n_layers, F1, same_pix)
+    assert np.array_equal(a["pyr"][sel], b["pyr"][sel])
+    del Rasterizer
