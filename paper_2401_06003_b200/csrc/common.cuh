@@ -205,8 +205,10 @@ __device__ __forceinline__ int pair_slot(const Params& P, const PointPairs& pp, 
 // u64 compare-exchange: (a, b) <- (min, max)
 __device__ __forceinline__ void cswap(uint64_t& a, uint64_t& b)
 {
-    const uint64_t lo = a < b ? a : b;
-    const uint64_t hi = a < b ? b : a;
+    // one 64-bit compare feeding both selects (nvcc otherwise emits a second, GT, compare)
+    uint64_t lo, hi;
+    asm("{\n\t.reg .pred p;\n\tsetp.lt.u64 p, %2, %3;\n\tselp.b64 %0, %2, %3, p;\n\tselp.b64 %1, %3, %2, p;\n\t}"
+        : "=l"(lo), "=l"(hi) : "l"(a), "l"(b));
     a = lo; b = hi;
 }
 

@@ -18,6 +18,7 @@ namespace trips {
 constexpr int kChunk = 512;                 // (point, tile) pairs staged per K4 iteration
 constexpr int kPairsPerThread = kChunk / kTilePix;
 constexpr int kBatch = 4;                   // record gathers issued together (memory-level parallelism)
+constexpr int kBlendBatch = 2;              // same in k_raster's blend (register budget: 3 CTAs/SM)
 
 __device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d)
 {
@@ -122,11 +123,13 @@ __device__ __forceinline__ TileCoord tile_coord(const Params& P, int t)
 // --------------------------------------------------------------------------- K4 raster
 
 template <int FC>
-__global__ void __launch_bounds__(kTilePix, 2) k_raster(Params P, float* __restrict__ pyramid, int save)
+__global__ void __launch_bounds__(kTilePix, 3) k_raster(Params P, float* __restrict__ pyramid, int save)
 {
     __shared__ uint64_t s_keys[kChunk * 4];
     __shared__ uint32_t s_cnt[kTilePix];
     __shared__ uint32_t s_base[kTilePix];
+    __shared__ uint32_t s_rej[kTilePix];             // fragments rejected by the threshold
+    __shared__ uint64_t s_thr[kTilePix];             // per-pixel 16th smallest key so far
     __shared__ uint32_t s_warp[32];
 
     const int t = blockIdx.x;
@@ -144,30 +147,46 @@ __global__ void __launch_bounds__(kTilePix, 2) k_raster(Params P, float* __restr
     for (int j = 0; j < 16; ++j) r[j] = kKeyMax;
     uint32_t total = 0;
 
-    for (uint32_t c0 = b0; c0 < b1; c0 += kChunk) {
-        const int m = (int)min((uint32_t)kChunk, b1 - c0);
+    s_thr[tid] = kKeyMax;
+    // Chunks interleave the bin (chunk ch takes positions ch, ch + nch, ...): a pixel's
+    // fragments then spread evenly over the chunks whatever the point order, which balances
+    // the per-pixel merge work inside a chunk and lets the 16th-key threshold of earlier
+    // chunks reject most fragments of later ones.
+    const uint32_t M = b1 - b0;
+    const uint32_t nch = (M + kChunk - 1) / kChunk;
+    for (uint32_t ch = 0; ch < nch; ++ch) {
+        const int m = (int)((M - ch + nch - 1) / nch);
+        const uint32_t c0 = b0 + ch;                 // element j of this chunk: c0 + j * nch
         s_cnt[tid] = 0;
+        s_rej[tid] = 0;
         __syncthreads();
-        // phase A: this chunk's pairs -> fragments of this tile (footprint origin in the bin)
-        uint64_t fk[kPairsPerThread][4];
+        // phase A: this chunk's pairs -> fragments of this tile (footprint origin in the bin).
+        // Lanes of a warp take pairs 8 apart: consecutive bin entries of a spatially ordered
+        // cloud hit the same pixels, and same-address shared atomics within a warp serialise.
         uint32_t fq[kPairsPerThread][4];             // (q | rank << 8), 0xffffffff = none
+        const int jl = (tid & 31) * 8 + (tid >> 5);
 #pragma unroll
         for (int k = 0; k < kPairsPerThread; ++k) {
 #pragma unroll
             for (int c = 0; c < 4; ++c) fq[k][c] = 0xffffffffu;
-            const int j = tid + k * kTilePix;
+            const int j = jl + k * kTilePix;
             if (j < m) {
-                const uint64_t key = P.bin_key[c0 + j];
-                const uint32_t o = P.bin_orig[c0 + j];
+                const uint64_t key = P.bin_key[c0 + (size_t)j * nch];
+                const uint32_t o = P.bin_orig[c0 + (size_t)j * nch];
                 const int qx0 = (int)(o & 31u) - 1, qy0 = (int)(o >> 5) - 1;
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
                     const int qx = qx0 + (c & 1), qy = qy0 + (c >> 1);
                     if (qx >= 0 && qx < kTile && qy >= 0 && qy < kTile && x_lo + qx < G.W && y_lo + qy < G.H) {
                         const uint32_t q = (uint32_t)(qy * kTile + qx);
-                        const uint32_t rank = atomicAdd(&s_cnt[q], 1u);
-                        fk[k][c] = key;
-                        fq[k][c] = q | (rank << 8);
+                        if (key >= s_thr[q]) {
+                            // cannot enter this pixel's top-16 any more (keys are unique):
+                            // counted for the list length, never sorted
+                            atomicAdd(&s_rej[q], 1u);
+                        } else {
+                            const uint32_t rank = atomicAdd(&s_cnt[q], 1u);
+                            fq[k][c] = q | (rank << 8);
+                        }
                     }
                 }
             }
@@ -178,12 +197,18 @@ __global__ void __launch_bounds__(kTilePix, 2) k_raster(Params P, float* __restr
         const uint32_t my_base = block_excl_scan(my_cnt, s_warp, &chunk_total);
         s_base[tid] = my_base;
         __syncthreads();
-        // phase B: counting-sort scatter by pixel
+        // phase B: counting-sort scatter by pixel (keys re-read from L1 instead of being held
+        // in registers across the scan)
 #pragma unroll
-        for (int k = 0; k < kPairsPerThread; ++k)
+        for (int k = 0; k < kPairsPerThread; ++k) {
+            const int j = jl + k * kTilePix;
+            if (j < m) {
+                const uint64_t key = P.bin_key[c0 + (size_t)j * nch];
 #pragma unroll
-            for (int c = 0; c < 4; ++c)
-                if (fq[k][c] != 0xffffffffu) s_keys[s_base[fq[k][c] & 0xffu] + (fq[k][c] >> 8)] = fk[k][c];
+                for (int c = 0; c < 4; ++c)
+                    if (fq[k][c] != 0xffffffffu) s_keys[s_base[fq[k][c] & 0xffu] + (fq[k][c] >> 8)] = key;
+            }
+        }
         __syncthreads();
         // phase C: merge this pixel's new fragments into its running top-16.  Network sizes are
         // chosen per warp (8 when no lane of the warp has more than 8 keys left in the group).
@@ -214,7 +239,8 @@ __global__ void __launch_bounds__(kTilePix, 2) k_raster(Params P, float* __restr
                 }
             }
         }
-        total += my_cnt;
+        total += my_cnt + s_rej[tid];
+        s_thr[tid] = r[15];                          // 16th smallest key so far (MAX if < 16)
         __syncthreads();
     }
 
@@ -230,20 +256,20 @@ __global__ void __launch_bounds__(kTilePix, 2) k_raster(Params P, float* __restr
     for (int c = 0; c < FC; ++c) C[c] = 0.f;
     float A = 0.f, T = 1.f;
 #pragma unroll
-    for (int b = 0; b < kCap / kBatch; ++b) {
-        if (b * kBatch >= K || (!save && T == 0.f)) break;
-        float4 rb[kBatch][1 + FC / 4];
+    for (int b = 0; b < kCap / kBlendBatch; ++b) {
+        if (b * kBlendBatch >= K || (!save && T == 0.f)) break;
+        float4 rb[kBlendBatch][1 + FC / 4];
 #pragma unroll
-        for (int u = 0; u < kBatch; ++u) {
-            const int mm = b * kBatch + u;                       // compile-time register index
+        for (int u = 0; u < kBlendBatch; ++u) {
+            const int mm = b * kBlendBatch + u;                  // compile-time register index
             const uint32_t ii = (uint32_t)(mm < K ? r[mm] : r[0]);
             const float4* rp = reinterpret_cast<const float4*>(P.rec + (size_t)ii * P.RS);
 #pragma unroll
             for (int c4 = 0; c4 <= FC / 4; ++c4) rb[u][c4] = __ldg(rp + c4);
         }
 #pragma unroll
-        for (int u = 0; u < kBatch; ++u) {
-            const int mm = b * kBatch + u;
+        for (int u = 0; u < kBlendBatch; ++u) {
+            const int mm = b * kBlendBatch + u;
             if (mm < K) {
                 const FragW w = frag_weights(rb[u][0], tc.l, P.n_layers, px, py);
                 const float tg = T * w.gamma;
