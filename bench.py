@@ -174,6 +174,7 @@ def run_cuda(args, rank, world, local_rank):
     import torch.distributed as dist
 
     from paper_2401_06003_b200 import Rasterizer, _abi
+    from paper_2401_06003_b200 import dist as tdist
     from synth import scenes
 
     dev = torch.device("cuda", local_rank)
@@ -186,26 +187,45 @@ def run_cuda(args, rank, world, local_rank):
     host = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory()
             for k, v in (("pos", sc.pos), ("sw", sc.sw), ("alpha", sc.alpha), ("desc", sc.desc))}
     d = {k: v.to(dev, non_blocking=True) for k, v in host.items()}
+    Gp = torch.from_numpy(scenes.grad_pyramid(rast.pyramid_floats, seed=100)).to(dev)
+    grad = torch.zeros(n, rast.G, dtype=torch.float32, device=dev)
+    my_views = tdist.shard_views(N_VIEWS, rank, world)
+    stream = torch.cuda.current_stream()
+
+    def step(dv, grad_buf):
+        render_view = tdist.cuda_view_renderer(rast, sc.cams, dv["pos"], dv["sw"], dv["alpha"], dv["desc"], Gp)
+        tdist.batch_step(render_view, my_views, grad_buf, world=world)
+
+    def timed_ms(dv, steps):
+        """device ms per step (CUDA events on the launching stream), max over ranks"""
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(steps):
+            step(dv, grad)
+        b.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([a.elapsed_time(b) / steps], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    random_order = None
     if args.order == "lib-morton":
+        if not args.no_random_order:
+            # side measurement: the same workload in the generator's (random) point order
+            for _ in range(2):
+                step(d, grad)
+            ms_r = timed_ms(d, 3)
+            random_order = {"value": N_VIEWS / (ms_r * 1e-3), "ms_per_step": ms_r, "steps": 3, "warmup": 2}
         # one-time data layout at load: the library's Morton permutation applied to every
         # per-point array (the cloud then lives in this order for the whole run)
         from paper_2401_06003_b200 import morton_order
         perm = morton_order(d["pos"])
         d = {k: v[perm].contiguous() for k, v in d.items()}
         host = {k: v.cpu().pin_memory() for k, v in d.items()}
-    Gp = torch.from_numpy(scenes.grad_pyramid(rast.pyramid_floats, seed=100)).to(dev)
-    grad = torch.zeros(n, rast.G, dtype=torch.float32, device=dev)
-    my_views = list(range(rank, N_VIEWS, world))
-    stream = torch.cuda.current_stream()
-
-    def step(dv, grad_buf):
-        grad_buf.zero_()
-        for v in my_views:
-            rast.project(sc.cams[v], dv["pos"], dv["sw"], dv["alpha"], dv["desc"])
-            rast.forward(save=True)
-            rast.backward(Gp, grad_buf)
-        if world > 1:
-            dist.all_reduce(grad_buf, op=dist.ReduceOp.SUM)
 
     # per-view statistics (deterministic; read outside the timed region)
     view_stats = []
@@ -311,6 +331,8 @@ def run_cuda(args, rank, world, local_rank):
         }
         if clk is not None:
             line["clocks"] = clk
+        if random_order is not None:
+            line["random_point_order"] = random_order
         if world == 1 and not args.no_cpu_baseline:
             from oracle import oracle as _o  # noqa: F401  (cpu_baseline leg only)
             t = [oracle_sample(sc, sc.cams[k], phase=k + 3) for k in range(2)]
@@ -328,24 +350,21 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
-    ap.add_argument("--order", default="random", choices=["random", "morton", "lib-morton"],
+    ap.add_argument("--order", default="lib-morton", choices=["random", "morton", "lib-morton"],
                     help="point order: as generated (random), numpy Morton sort, or the library's "
                          "trips_morton_order applied once at load (outside the timed region)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-random-order", action="store_true", help="skip the random-order side measurement")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
-    if world > 1:
-        import torch
-        import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    from paper_2401_06003_b200 import dist as tdist
+    rank, world, local_rank = tdist.init_from_env("nccl")
     run_cuda(args, rank, world, local_rank)
     if world > 1:
         import torch.distributed as dist

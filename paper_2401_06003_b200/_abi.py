@@ -9,7 +9,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtrips.so")
+# TRIPS_LIB overrides the library path (kernel experiments build variants elsewhere)
+LIB_PATH = os.environ.get("TRIPS_LIB", os.path.join(_HERE, "libtrips.so"))
 
 TRIPS_OK = 0
 TRIPS_ERR_ARG = -1
