@@ -6,13 +6,14 @@
 // This build privatises the counters instead.  A persistent grid of C CTAs splits the points
 // into C contiguous ranges; every CTA keeps one counter per pyramid tile in shared memory:
 //
-//   k_count  per CTA: project its points (Sec. 3.1, Eq. 2), enumerate their (point, tile)
+//   k_count  per CTA: project its points (Sec. 3.1, Eq. 2), write their screen records,
+//            enumerate their (point, tile)
 //            pairs (Eq. 4 layers, 2x2 footprints), count them per tile in shared memory;
 //            then reserve its slice of each touched tile with ONE global atomic per (CTA,
 //            tile) on the tile total; the returned base goes to hist[c][t]
 //   k_tscan  one CTA: exclusive scan of the tile totals -> tile_off; kept-list capacity base
-//   k_emit   per CTA, same point range: project again (bit-identical), write the screen
-//            record, place every pair at tile_off[t] + hist[c][t] + (shared-memory cursor)
+//   k_emit   per CTA, same point range: re-enumerate the pairs from the screen record and
+//            place every pair at tile_off[t] + hist[c][t] + (shared-memory cursor)
 //
 // The order of pairs inside a tile's bin is not defined; K4 orders fragments by the full
 // (z, i) key (reading Q12), so results do not depend on it.
@@ -66,7 +67,11 @@ __device__ __forceinline__ void cta_range(int n, int& b, int& e)
 
 // --------------------------------------------------------------------------- k_count
 
-__global__ void __launch_bounds__(kBinThreads) k_count(Params P)
+// Projects every point once (exact block), writes its screen record and depth, and counts its
+// (point, tile) pairs in shared-memory counters.
+template <int FC>
+__global__ void __launch_bounds__(kBinThreads) k_count(Params P, int8_t* __restrict__ level_out,
+                                                       float* __restrict__ proj_out)
 {
     extern __shared__ __align__(16) uint32_t s_hist[];            // [T]
     __shared__ uint32_t s_v;
@@ -78,16 +83,32 @@ __global__ void __launch_bounds__(kBinThreads) k_count(Params P)
     uint32_t nvis = 0;
     for (int i = b + threadIdx.x; i < e; i += blockDim.x) {
         const float* q = P.pos + 3 * (size_t)i;
-        float xs, ys, z, s;
-        if (project_exact(P.cam, __ldg(q), __ldg(q + 1), __ldg(q + 2), __ldg(P.sw + i), xs, ys, z, s)) {
-            ++nvis;
-            const PointPairs pp = point_pairs(P, xs, ys, s);
+        float xs = 0.f, ys = 0.f, z = 0.f, s = 0.f;
+        const bool vis = project_exact(P.cam, __ldg(q), __ldg(q + 1), __ldg(q + 2), __ldg(P.sw + i), xs, ys, z, s);
+        float4* r = reinterpret_cast<float4*>(P.rec + (size_t)i * P.RS);
+        r[0] = make_float4(vis ? xs : 0.f, vis ? ys : 0.f, vis ? s : kCulled, __ldg(P.alpha + i));
+        const float* d = P.desc + (size_t)i * P.F;
+        if (P.F == FC && (reinterpret_cast<uintptr_t>(d) & 15) == 0) {
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                uint32_t o;
-                const int t = pair_slot(P, pp, k, o);
-                if (t >= 0) atomicAdd(&s_hist[t], 1u);
+            for (int c = 0; c < FC / 4; ++c) r[1 + c] = __ldg(reinterpret_cast<const float4*>(d) + c);
+        } else {
+#pragma unroll
+            for (int c = 0; c < FC / 4; ++c) {
+                float v[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) v[j] = (4 * c + j < P.F) ? __ldg(d + 4 * c + j) : 0.f;
+                r[1 + c] = make_float4(v[0], v[1], v[2], v[3]);
             }
+        }
+        P.zbuf[i] = z;
+        if (level_out) level_out[i] = (int8_t)(vis ? select_levels(s, P.n_layers).code : -1);
+        if (proj_out) {
+            const float nan = __int_as_float(0x7fc00000);
+            reinterpret_cast<float4*>(proj_out)[i] = vis ? make_float4(xs, ys, z, s) : make_float4(nan, nan, nan, nan);
+        }
+        if (vis) {
+            ++nvis;
+            for_each_pair(P, xs, ys, s, [&](int t, uint32_t) { atomicAdd(&s_hist[t], 1u); });
         }
     }
     const uint32_t wv = __reduce_add_sync(0xffffffffu, nvis);
@@ -135,54 +156,26 @@ __global__ void __launch_bounds__(1024) k_tscan(Params P)
 
 // --------------------------------------------------------------------------- k_emit
 
-template <int FC>
-__global__ void __launch_bounds__(kBinThreads) k_emit(Params P, int8_t* __restrict__ level_out,
-                                                      float* __restrict__ proj_out)
+// Same point partition as k_count: re-enumerates each visible point's pairs from its screen
+// record (no projection) and places them at tile_off[t] + this CTA's slice + shared cursor.
+__global__ void __launch_bounds__(kBinThreads) k_emit(Params P)
 {
     extern __shared__ __align__(16) uint32_t s_cur[];             // [T] fill cursors
     const uint32_t* row = P.hist + (size_t)blockIdx.x * P.T;
-    for (int t = threadIdx.x; t < P.T; t += blockDim.x) s_cur[t] = P.tile_off[t] + row[t];   // garbage for tiles
-                                                                  // this CTA never touches
+    // entries of tiles this CTA never touches are garbage and never used
+    for (int t = threadIdx.x; t < P.T; t += blockDim.x) s_cur[t] = P.tile_off[t] + row[t];
     __syncthreads();
     int b, e;
     cta_range(P.n, b, e);
     for (int i = b + threadIdx.x; i < e; i += blockDim.x) {
-        float xs = 0.f, ys = 0.f, z = 0.f, s = 0.f;
-        const float* q = P.pos + 3 * (size_t)i;
-        const bool vis = project_exact(P.cam, __ldg(q), __ldg(q + 1), __ldg(q + 2), __ldg(P.sw + i), xs, ys, z, s);
-        float4* r = reinterpret_cast<float4*>(P.rec + (size_t)i * P.RS);
-        r[0] = make_float4(vis ? xs : 0.f, vis ? ys : 0.f, vis ? s : kCulled, __ldg(P.alpha + i));
-        const float* d = P.desc + (size_t)i * P.F;
-        if (P.F == FC && (reinterpret_cast<uintptr_t>(d) & 15) == 0) {
-#pragma unroll
-            for (int c = 0; c < FC / 4; ++c) r[1 + c] = __ldg(reinterpret_cast<const float4*>(d) + c);
-        } else {
-#pragma unroll
-            for (int c = 0; c < FC / 4; ++c) {
-                float v[4];
-#pragma unroll
-                for (int j = 0; j < 4; ++j) v[j] = (4 * c + j < P.F) ? __ldg(d + 4 * c + j) : 0.f;
-                r[1 + c] = make_float4(v[0], v[1], v[2], v[3]);
-            }
-        }
-        if (level_out) level_out[i] = (int8_t)(vis ? select_levels(s, P.n_layers).code : -1);
-        if (proj_out) {
-            const float nan = __int_as_float(0x7fc00000);
-            reinterpret_cast<float4*>(proj_out)[i] = vis ? make_float4(xs, ys, z, s) : make_float4(nan, nan, nan, nan);
-        }
-        if (!vis) continue;
-        const uint64_t key = ((uint64_t)__float_as_uint(z) << 32) | (uint32_t)i;
-        const PointPairs pp = point_pairs(P, xs, ys, s);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            uint32_t o;
-            const int t = pair_slot(P, pp, k, o);
-            if (t >= 0) {
-                const uint32_t pos = atomicAdd(&s_cur[t], 1u);
-                P.bin_key[pos] = key;
-                P.bin_orig[pos] = (uint16_t)o;
-            }
-        }
+        const float4 r0 = __ldg(reinterpret_cast<const float4*>(P.rec + (size_t)i * P.RS));
+        if (!(r0.z >= 0.f)) continue;                             // culled
+        const uint64_t key = ((uint64_t)__float_as_uint(__ldg(P.zbuf + i)) << 32) | (uint32_t)i;
+        for_each_pair(P, r0.x, r0.y, r0.z, [&](int t, uint32_t o) {
+            const uint32_t pos = atomicAdd(&s_cur[t], 1u);
+            P.bin_key[pos] = key;
+            P.bin_orig[pos] = (uint16_t)o;
+        });
     }
 }
 

@@ -45,6 +45,7 @@ struct Params {
     const float* pos; const float* sw; const float* alpha; const float* desc;
     // workspace
     float* rec;            // [n][RS]  (x, y, s, alpha, tau[FC])     s < 0 marks culled
+    float* zbuf;           // [n]      view depth z
     uint32_t* hist;        // [C][T]   per-CTA tile counts -> per-CTA offsets within the tile
     uint32_t* cta_vis;     // [C]      visible points per binning CTA (statistics)
     uint32_t* tile_off;    // [T+1]    first pair of each tile's bin; [T] = number of pairs M
@@ -200,6 +201,28 @@ __device__ __forceinline__ int pair_slot(const Params& P, const PointPairs& pp, 
     const int tx = pp.tx0[ls] + dx, ty = pp.ty0[ls] + dy;
     orig = (uint32_t)(pp.x0[ls] - tx * 16 + 1) | ((uint32_t)(pp.y0[ls] - ty * 16 + 1) << 5);
     return G.tile_base + ty * G.tiles_x + tx;
+}
+
+// Calls fn(tile, orig) for every (point, tile) pair of a point (same pairs as the slot form
+// above, without evaluating empty slots): per selected layer, the tiles touched by the
+// in-bounds pixels of the 2x2 footprint; orig = footprint origin relative to the tile.
+template <class Fn>
+__device__ __forceinline__ void for_each_pair(const Params& P, float xs, float ys, float s, Fn&& fn)
+{
+    const Levels lv = select_levels(s, P.n_layers);
+    for (int k = 0; k < lv.n; ++k) {
+        const int l = lv.lo + k;
+        const LayerGeom& G = P.L[l];
+        Foot f;
+        if (!footprint(xs, ys, l, G.W, G.H, f)) continue;
+        const int xa = max(f.x0, 0), xb = min(f.x0 + 1, G.W - 1);
+        const int ya = max(f.y0, 0), yb = min(f.y0 + 1, G.H - 1);
+        if (xa > xb || ya > yb) continue;
+        for (int ty = ya >> 4; ty <= (yb >> 4); ++ty)
+            for (int tx = xa >> 4; tx <= (xb >> 4); ++tx)
+                fn(G.tile_base + ty * G.tiles_x + tx,
+                   (uint32_t)(f.x0 - tx * 16 + 1) | ((uint32_t)(f.y0 - ty * 16 + 1) << 5));
+    }
 }
 
 // u64 compare-exchange: (a, b) <- (min, max)

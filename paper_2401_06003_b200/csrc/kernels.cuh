@@ -15,10 +15,19 @@
 
 namespace trips {
 
-constexpr int kChunk = 512;                 // (point, tile) pairs staged per K4 iteration
+#ifndef TRIPS_CHUNK
+#define TRIPS_CHUNK 1024
+#endif
+#ifndef TRIPS_BLEND_BATCH
+#define TRIPS_BLEND_BATCH 2
+#endif
+#ifndef TRIPS_RASTER_CTAS
+#define TRIPS_RASTER_CTAS 3
+#endif
+constexpr int kChunk = TRIPS_CHUNK;         // (point, tile) pairs staged per K4 iteration
 constexpr int kPairsPerThread = kChunk / kTilePix;
 constexpr int kBatch = 4;                   // record gathers issued together (memory-level parallelism)
-constexpr int kBlendBatch = 2;              // same in k_raster's blend (register budget: 3 CTAs/SM)
+constexpr int kBlendBatch = TRIPS_BLEND_BATCH;  // same in k_raster's blend (register budget: 3 CTAs/SM)
 
 __device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d)
 {
@@ -127,7 +136,7 @@ __device__ __forceinline__ TileCoord tile_coord(const Params& P, int t)
 // --------------------------------------------------------------------------- K4 raster
 
 template <int FC>
-__global__ void __launch_bounds__(kTilePix, 3) k_raster(Params P, float* __restrict__ pyramid, int save)
+__global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P, float* __restrict__ pyramid, int save)
 {
     __shared__ uint64_t s_keys[kChunk * 4];
     __shared__ uint32_t s_cnt[kTilePix];

@@ -37,7 +37,7 @@ struct trips_plan {
     uint64_t kcap;
     // workspace layout (byte offsets)
     int32_t ctas;           // binning CTAs (persistent grid)
-    size_t off_rec, off_hist, off_cvis, off_toff, off_tkb, off_bkey, off_borig, off_pcnt, off_pmeta, off_kept, off_kgam,
+    size_t off_rec, off_z, off_hist, off_cvis, off_toff, off_tkb, off_bkey, off_borig, off_pcnt, off_pmeta, off_kept, off_kgam,
         off_stats, ws_bytes;
     // state
     const void* ws_bound = nullptr;
@@ -112,7 +112,7 @@ int num_sms()
 template <int FC>
 int set_emit_attr(size_t bytes)
 {
-    return (int)cudaFuncSetAttribute(k_emit<FC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    return (int)cudaFuncSetAttribute(k_count<FC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
 // Opt the binning kernels into > 48 KB of dynamic shared memory (one counter per tile).
@@ -120,7 +120,7 @@ int set_smem_attrs(size_t bytes)
 {
     static size_t done = 0;
     if (bytes <= done) return TRIPS_OK;
-    cudaError_t e = cudaFuncSetAttribute(k_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    cudaError_t e = cudaFuncSetAttribute(k_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     int bad = (int)e;
     bad |= set_emit_attr<4>(bytes) | set_emit_attr<8>(bytes) | set_emit_attr<12>(bytes) | set_emit_attr<16>(bytes) |
            set_emit_attr<20>(bytes) | set_emit_attr<24>(bytes) | set_emit_attr<28>(bytes) | set_emit_attr<32>(bytes);
@@ -146,6 +146,7 @@ Params make_params(const trips_plan* p, void* ws)
     P.cam = p->cam;
     char* b = static_cast<char*>(ws);
     P.rec = reinterpret_cast<float*>(b + p->off_rec);
+    P.zbuf = reinterpret_cast<float*>(b + p->off_z);
     P.hist = reinterpret_cast<uint32_t*>(b + p->off_hist);
     P.cta_vis = reinterpret_cast<uint32_t*>(b + p->off_cvis);
     P.tile_off = reinterpret_cast<uint32_t*>(b + p->off_toff);
@@ -216,6 +217,7 @@ int trips_plan_create(const trips_config* cfg, int32_t width, int32_t height, in
     size_t o = 0;
     p->ctas = num_sms() * kBinCtasPerSm;
     p->off_rec = o;    o = align256(o + N * p->RS * sizeof(float));
+    p->off_z = o;      o = align256(o + N * sizeof(float));
     p->off_hist = o;   o = align256(o + (size_t)p->ctas * tiles * 4);
     p->off_cvis = o;   o = align256(o + (size_t)p->ctas * 4);
     p->off_toff = o;   o = align256(o + ((size_t)tiles + 1) * 4);
@@ -288,14 +290,14 @@ int trips_project(trips_plan* p, void* ws, const trips_camera* c, int64_t n, con
     if ((rc = set_smem_attrs(hsm))) return rc;
     {
         StageScope sc(p, 0, st);
-        k_count<<<p->ctas, kBinThreads, hsm, st>>>(P);
+        TRIPS_FC_SWITCH(p->FC, (k_count<kFC><<<p->ctas, kBinThreads, hsm, st>>>(P, level_out, proj_out)));
         if ((rc = check_launch())) return rc;
         k_tscan<<<1, 1024, 0, st>>>(P);
         if ((rc = check_launch())) return rc;
     }
     {
         StageScope sc(p, 1, st);
-        TRIPS_FC_SWITCH(p->FC, (k_emit<kFC><<<p->ctas, kBinThreads, hsm, st>>>(P, level_out, proj_out)));
+        k_emit<<<p->ctas, kBinThreads, hsm, st>>>(P);
         if ((rc = check_launch())) return rc;
     }
     p->stage = 1;
