@@ -148,7 +148,9 @@ def run_reference(args, rank, world):
     from synth import scenes
     if rank != 0:
         return
-    sc = scenes.make_config("C4", n=N_POINTS, n_views=N_VIEWS, order=args.order)
+    # lib-morton: the same Morton layout, computed by the generator (the oracle has no GPU)
+    sc = scenes.make_config("C4", n=N_POINTS, n_views=N_VIEWS,
+                            order="morton" if args.order == "lib-morton" else args.order)
     for w in range(args.warmup):
         oracle_sample(sc, sc.cams[w % N_VIEWS], phase=w)
     times = [oracle_sample(sc, sc.cams[(args.warmup + k) % N_VIEWS], phase=k) for k in range(args.steps)]
