@@ -81,16 +81,37 @@ __global__ void __launch_bounds__(kBinThreads) k_count(Params P, int8_t* __restr
     int b, e;
     cta_range(P.n, b, e);
     uint32_t nvis = 0;
-    for (int i = b + threadIdx.x; i < e; i += blockDim.x) {
-        const float* q = P.pos + 3 * (size_t)i;
-        float xs = 0.f, ys = 0.f, z = 0.f, s = 0.f;
-        const bool vis = project_exact(P.cam, __ldg(q), __ldg(q + 1), __ldg(q + 2), __ldg(P.sw + i), xs, ys, z, s);
-        float4* r = reinterpret_cast<float4*>(P.rec + (size_t)i * P.RS);
-        r[0] = make_float4(vis ? xs : 0.f, vis ? ys : 0.f, vis ? s : kCulled, __ldg(P.alpha + i));
-        const float* d = P.desc + (size_t)i * P.F;
-        if (P.F == FC && (reinterpret_cast<uintptr_t>(d) & 15) == 0) {
+#ifndef TRIPS_COUNT_UNROLL
+#define TRIPS_COUNT_UNROLL 1
+#endif
+    constexpr int kU = TRIPS_COUNT_UNROLL;        // points per thread per iteration (loads issued together)
+    const bool vec_desc = P.F == FC && (reinterpret_cast<uintptr_t>(P.desc) & 15) == 0;
+    for (int i0 = b + threadIdx.x; i0 < e; i0 += kU * blockDim.x) {
+      float in[kU][6];
+      float4 dv[kU][FC / 4];
 #pragma unroll
-            for (int c = 0; c < FC / 4; ++c) r[1 + c] = __ldg(reinterpret_cast<const float4*>(d) + c);
+      for (int u = 0; u < kU; ++u) {
+        const int i = min(i0 + u * (int)blockDim.x, e - 1);
+        const float* q = P.pos + 3 * (size_t)i;
+        in[u][0] = __ldg(q); in[u][1] = __ldg(q + 1); in[u][2] = __ldg(q + 2);
+        in[u][3] = __ldg(P.sw + i); in[u][4] = __ldg(P.alpha + i);
+        if (vec_desc) {
+#pragma unroll
+            for (int c = 0; c < FC / 4; ++c) dv[u][c] = __ldg(reinterpret_cast<const float4*>(P.desc + (size_t)i * P.F) + c);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int i = i0 + u * (int)blockDim.x;
+        if (i >= e) break;
+        float xs = 0.f, ys = 0.f, z = 0.f, s = 0.f;
+        const bool vis = project_exact(P.cam, in[u][0], in[u][1], in[u][2], in[u][3], xs, ys, z, s);
+        float4* r = reinterpret_cast<float4*>(P.rec + (size_t)i * P.RS);
+        r[0] = make_float4(vis ? xs : 0.f, vis ? ys : 0.f, vis ? s : kCulled, in[u][4]);
+        const float* d = P.desc + (size_t)i * P.F;
+        if (vec_desc) {
+#pragma unroll
+            for (int c = 0; c < FC / 4; ++c) r[1 + c] = dv[u][c];
         } else {
 #pragma unroll
             for (int c = 0; c < FC / 4; ++c) {
@@ -110,15 +131,25 @@ __global__ void __launch_bounds__(kBinThreads) k_count(Params P, int8_t* __restr
             ++nvis;
             for_each_pair(P, xs, ys, s, [&](int t, uint32_t) { atomicAdd(&s_hist[t], 1u); });
         }
+      }
     }
     const uint32_t wv = __reduce_add_sync(0xffffffffu, nvis);
     if (lane_id() == 0 && wv) atomicAdd(&s_v, wv);
     __syncthreads();
     // reserve this CTA's slice of every tile it touches: tile_off[t] holds the running tile
     // total here (k_tscan turns totals into offsets); the returned value is the CTA's offset
-    // inside the tile.  One atomic per (CTA, non-empty tile), spread over T addresses.
+    // inside the tile.  One atomic per (CTA, non-empty tile), spread over T addresses; every
+    // CTA starts at a different tile so that CTAs finishing together do not queue on the
+    // same addresses (a randomly ordered cloud touches almost every tile from every CTA).
     uint32_t* row = P.hist + (size_t)blockIdx.x * P.T;
-    for (int t = threadIdx.x; t < P.T; t += blockDim.x) {
+#ifdef TRIPS_FLUSH_ROT
+    const int rot = (int)(((uint64_t)blockIdx.x * P.T) / gridDim.x);
+#else
+    const int rot = 0;
+#endif
+    for (int k = threadIdx.x; k < P.T; k += blockDim.x) {
+        int t = k + rot;
+        if (t >= P.T) t -= P.T;
         const uint32_t c = s_hist[t];
         if (c) row[t] = atomicAdd(&P.tile_off[t], c);
     }
