@@ -148,10 +148,14 @@ int trips_splat_forward(trips_plan* plan, void* ws, float* pyramid, uint32_t fla
 /* Backward of the last saved forward.  grad_pyramid has the pyramid layout (16-B aligned).
  * Gradients are ACCUMULATED (+=) into grad[n][G] (G = trips_grad_stride, 16-B aligned),
  * so several views sum into one buffer (reading Q21); the caller zeroes it once per batch.
+ * grad_camera (nullable, device float[17], 4-B aligned) receives += the gradient w.r.t. the
+ * camera of the last trips_project (the paper optimises camera parameters):
+ * (dR00..dR22 row-major, dt0..dt2, dfx, dfy, dcx, dcy, df) for p = R x + t, x = fx p_x/z + cx,
+ * y = fy p_y/z + cy, s = f s_w/z.  Passing NULL costs nothing.
  * May be called more than once per forward.  Errors: TRIPS_ERR_STATE (last forward not
  * saved, or ws differs), TRIPS_ERR_ARG, TRIPS_ERR_ALIGN, TRIPS_ERR_CUDA. */
 int trips_splat_backward(trips_plan* plan, void* ws, const float* grad_pyramid, float* grad,
-                         void* stream);
+                         float* grad_camera, void* stream);
 
 /* ---- introspection ----------------------------------------------------------------- */
 

@@ -39,7 +39,7 @@ def _lib(real: str):
                                        vp, vp, vp, vp, vp, C.POINTER(_Stats)]
         lib.oracle_backward.restype = C.c_int
         lib.oracle_backward.argtypes = [C.POINTER(_Camera), C.c_int, C.c_int, C.c_int64, vp, vp, vp, vp,
-                                        vp, vp, vp, vp]
+                                        vp, vp, vp, vp, vp, vp]
         _LIBS[real] = lib
     return _LIBS[real]
 
@@ -138,11 +138,16 @@ def forward(cam, n_layers, pos, sw, alpha, desc, mask=None, real="float", want_k
     return dict(pyramid=pyr, mag=mag, counts=counts, kept=kept, stats=stats, F=F, P=P)
 
 
+CAMERA_GRAD_NAMES = ("R00", "R01", "R02", "R10", "R11", "R12", "R20", "R21", "R22", "t0", "t1", "t2",
+                     "fx", "fy", "cx", "cy", "f")
+
+
 def backward(cam, n_layers, pos, sw, alpha, desc, grad_pyramid, mask=None, real="float", grad=None,
-             grad_mag=None):
+             grad_mag=None, grad_cam=None, grad_cam_mag=None):
     """O1 backward.  Returns (grad [n, 5+F] float64, grad_mag [n, 5+F]); rows are
     (d/dx, d/dy, d/dz, d/ds_w, d/dalpha, d/dtau[F]).  If grad / grad_mag are given
-    they are accumulated into (multi-view sum, reading Q21)."""
+    they are accumulated into (multi-view sum, reading Q21).  grad_cam / grad_cam_mag
+    (float64 [17], CAMERA_GRAD_NAMES order) receive the camera gradient if given."""
     pos = _f32(pos, (-1, 3))
     n = pos.shape[0]
     sw = _f32(sw, (n,))
@@ -158,6 +163,6 @@ def backward(cam, n_layers, pos, sw, alpha, desc, grad_pyramid, mask=None, real=
     m = None if mask is None else np.ascontiguousarray(mask, dtype=np.uint8)
     rc = _lib(real).oracle_backward(C.byref(camera_struct(cam)), n_layers, F, n, _ptr(pos), _ptr(sw),
                                     _ptr(alpha), _ptr(desc), _ptr(gp), _ptr(grad), _ptr(grad_mag),
-                                    _ptr(m))
+                                    _ptr(m), _ptr(grad_cam), _ptr(grad_cam_mag))
     assert rc == 0, rc
     return grad, grad_mag

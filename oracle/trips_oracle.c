@@ -400,11 +400,14 @@ int oracle_forward(const oracle_camera* cam, int n_layers, int F, int64_t n, con
  *   grad     [n][5+F] double, row = (d/dx, d/dy, d/dz, d/ds_w, d/dalpha, d/dtau[F])
  *   grad_mag [n][5+F] double, nullable: the same chain with |.| of every factor
  *            (a scale for the rounding error of any evaluation order)
+ *   grad_cam [17] double, nullable: camera gradient (dR row-major, dt, dfx, dfy, dcx, dcy,
+ *            df), summed; grad_cam_mag its magnitude scale (nullable)
  * grad_pyramid has the pyramid layout (float).  mask as in oracle_forward.
  */
 int oracle_backward(const oracle_camera* cam, int n_layers, int F, int64_t n, const float* pos,
                     const float* sw, const float* alpha, const float* desc,
-                    const float* grad_pyramid, double* grad, double* grad_mag, const uint8_t* mask)
+                    const float* grad_pyramid, double* grad, double* grad_mag, const uint8_t* mask,
+                    double* grad_cam, double* grad_cam_mag)
 {
     if (n_layers < 1 || n_layers > 16 || F < 1 || F > 64 || n < 0) return -1;
     scene_t S;
@@ -507,6 +510,36 @@ int oracle_backward(const oracle_camera* cam, int n_layers, int F, int64_t n, co
         go[3] += gi[2] * (double)cam->f / z;                  /* d s / d s_w = f / z */
         go[4] += gi[3];
         for (int c = 0; c < F; ++c) go[5 + c] += gi[4 + c];
+        if (grad_cam) {
+            /* camera parameters (PAPER.md:92, 268 optimise them):
+             * [dR (9, row-major), dt (3), dfx, dfy, dcx, dcy, df], with p = R X + t,
+             * x = fx p_x / z + cx, y = fy p_y / z + cy, s = f s_w / z. */
+            const float* X = pos + 3 * i;
+            double pv[3];
+            for (int r = 0; r < 3; ++r)
+                pv[r] = (double)cam->R[3 * r] * X[0] + (double)cam->R[3 * r + 1] * X[1]
+                      + (double)cam->R[3 * r + 2] * X[2] + (double)cam->t[r];
+            for (int a = 0; a < 3; ++a) {
+                for (int b = 0; b < 3; ++b) grad_cam[3 * a + b] += gp[a] * (double)X[b];
+                grad_cam[9 + a] += gp[a];
+            }
+            grad_cam[12] += gi[0] * pv[0] / z;
+            grad_cam[13] += gi[1] * pv[1] / z;
+            grad_cam[14] += gi[0];
+            grad_cam[15] += gi[1];
+            grad_cam[16] += gi[2] * (double)sw[i] / z;
+            if (grad_cam_mag) {
+                for (int a = 0; a < 3; ++a) {
+                    for (int b = 0; b < 3; ++b) grad_cam_mag[3 * a + b] += mp[a] * fabs((double)X[b]);
+                    grad_cam_mag[9 + a] += mp[a];
+                }
+                grad_cam_mag[12] += mi[0] * fabs(pv[0]) / z;
+                grad_cam_mag[13] += mi[1] * fabs(pv[1]) / z;
+                grad_cam_mag[14] += mi[0];
+                grad_cam_mag[15] += mi[1];
+                grad_cam_mag[16] += mi[2] * fabs((double)sw[i]) / z;
+            }
+        }
         if (grad_mag) {
             double* mo = grad_mag + i * GO;
             for (int k = 0; k < 3; ++k)

@@ -63,7 +63,7 @@ SIGNATURES = [
     ("trips_project", C.c_int, [_VP, _VP, C.POINTER(trips_camera), C.c_int64, _VP, _VP, _VP, _VP, _VP, _VP,
                                 _VP]),
     ("trips_splat_forward", C.c_int, [_VP, _VP, _VP, C.c_uint32, _VP]),
-    ("trips_splat_backward", C.c_int, [_VP, _VP, _VP, _VP, _VP]),
+    ("trips_splat_backward", C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP]),
     ("trips_read_stats", C.c_int, [_VP, _VP, C.POINTER(trips_stats), _VP]),
     ("trips_debug_export", C.c_int, [_VP, _VP, C.c_int32, _VP, _VP]),
     ("trips_set_profiling", C.c_int, [_VP, C.c_int32]),
@@ -160,8 +160,8 @@ def trips_splat_forward(plan, ws, pyramid, flags, stream=None):
     return lib().trips_splat_forward(plan, ws, pyramid, flags, stream)
 
 
-def trips_splat_backward(plan, ws, grad_pyramid, grad, stream=None):
-    return lib().trips_splat_backward(plan, ws, grad_pyramid, grad, stream)
+def trips_splat_backward(plan, ws, grad_pyramid, grad, grad_camera=None, stream=None):
+    return lib().trips_splat_backward(plan, ws, grad_pyramid, grad, grad_camera, stream)
 
 
 def trips_read_stats(plan, ws, stream=None):

@@ -322,9 +322,11 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
 
 // --------------------------------------------------------------------------- K5 backward
 
-template <int FC>
+// CAM: also accumulate the camera gradient:
+// grad_cam[17] += (dR row-major, dt, dfx, dfy, dcx, dcy, df), one block reduction per tile.
+template <int FC, bool CAM>
 __global__ void __launch_bounds__(kTilePix) k_backward(Params P, const float* __restrict__ gpyr,
-                                                       float* __restrict__ grad)
+                                                       float* __restrict__ grad, float* __restrict__ grad_cam)
 {
     const int t = blockIdx.x;
     const TileCoord tc = tile_coord(P, t);
@@ -333,18 +335,21 @@ __global__ void __launch_bounds__(kTilePix) k_backward(Params P, const float* __
     const int px = tc.tx * kTile + (tid & (kTile - 1)), py = tc.ty * kTile + (tid >> 4);
     const uint32_t meta = P.pix_meta[(size_t)t * kTilePix + tid];
     const int K = (int)(meta & 31u);
-    if (K == 0) return;
+    if (!CAM && K == 0) return;
     const size_t kidx = (size_t)P.tile_kbase[t] + (meta >> 5);
     const uint64_t* kp = P.kept + kidx;
     const float* gm = P.kept_gamma + kidx;
+    float cg[CAM ? 17 : 1];
+#pragma unroll
+    for (int k = 0; k < (CAM ? 17 : 1); ++k) cg[k] = 0.f;
 
     // upstream gradient of this pixel: gC (F channels) and gA
     const int64_t plane = (int64_t)G.W * G.H;
     const float* gp = gpyr + G.float_off + (int64_t)py * G.W + px;
     float gC[FC];
 #pragma unroll
-    for (int c = 0; c < FC; ++c) gC[c] = (c < P.F) ? __ldg(gp + c * plane) : 0.f;
-    const float gA = __ldg(gp + P.F * plane);
+    for (int c = 0; c < FC; ++c) gC[c] = (K > 0 && c < P.F) ? __ldg(gp + c * plane) : 0.f;
+    const float gA = K > 0 ? __ldg(gp + P.F * plane) : 0.f;
 
     // T_m from the saved gamma_m (Eq. 6) -- no record gathers
     float gam[kCap], Tm[kCap];
@@ -411,6 +416,26 @@ __global__ void __launch_bounds__(kTilePix) k_backward(Params P, const float* __
             const float gY = cam.R[1] * gpx + cam.R[4] * gpy + cam.R[7] * gpz;
             const float gZ = cam.R[2] * gpx + cam.R[5] * gpy + cam.R[8] * gpz;
             const float gsw = gs * cam.f * iz;
+            if (CAM) {
+                // p = (px, py, z) from the screen record, X = R^T (p - t)
+                const float pxv = (r0.x - cam.cx) * z / cam.fx, pyv = (r0.y - cam.cy) * z / cam.fy;
+                const float q0 = pxv - cam.t[0], q1 = pyv - cam.t[1], q2 = z - cam.t[2];
+                const float Xw[3] = {cam.R[0] * q0 + cam.R[3] * q1 + cam.R[6] * q2,
+                                     cam.R[1] * q0 + cam.R[4] * q1 + cam.R[7] * q2,
+                                     cam.R[2] * q0 + cam.R[5] * q1 + cam.R[8] * q2};
+                const float gpv[3] = {gpx, gpy, gpz};
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+#pragma unroll
+                    for (int bb2 = 0; bb2 < 3; ++bb2) cg[3 * a + bb2] = fmaf(gpv[a], Xw[bb2], cg[3 * a + bb2]);
+                    cg[9 + a] += gpv[a];
+                }
+                cg[12] = fmaf(gxs, pxv * iz, cg[12]);
+                cg[13] = fmaf(gys, pyv * iz, cg[13]);
+                cg[14] += gxs;
+                cg[15] += gys;
+                cg[16] = fmaf(gs, r0.z / cam.f, cg[16]);
+            }
             float* grow = grad + (size_t)i * P.G;
             red_add_v4(grow, gX, gY, gZ, gsw);
             float v[FC + 4];
@@ -424,6 +449,24 @@ __global__ void __launch_bounds__(kTilePix) k_backward(Params P, const float* __
 #pragma unroll
             for (int c = 0; c < FC; ++c) B[c] = g * tau[c] + (1.0f - g) * B[c];
             bb = g + (1.0f - g) * bb;
+        }
+    }
+    if (CAM) {
+        // block reduction of the 17 camera-gradient partials, 17 atomics per tile
+        __shared__ float s_cg[kTilePix / 32][17];
+#pragma unroll
+        for (int k = 0; k < 17; ++k) {
+            float v = cg[k];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if ((tid & 31) == 0) s_cg[tid >> 5][k] = v;
+        }
+        __syncthreads();
+        if (tid < 17) {
+            float v = 0.f;
+#pragma unroll
+            for (int w = 0; w < kTilePix / 32; ++w) v += s_cg[w][tid];
+            if (v != 0.f) atomicAdd(grad_cam + tid, v);
         }
     }
 }

@@ -322,17 +322,24 @@ int trips_splat_forward(trips_plan* p, void* ws, float* pyramid, uint32_t flags,
     return TRIPS_OK;
 }
 
-int trips_splat_backward(trips_plan* p, void* ws, const float* grad_pyramid, float* grad, void* stream)
+int trips_splat_backward(trips_plan* p, void* ws, const float* grad_pyramid, float* grad, float* grad_camera,
+                         void* stream)
 {
     if (!p || !ws || !grad_pyramid || !grad) return TRIPS_ERR_ARG;
     if (p->stage != 2 || ws != p->ws_bound) return TRIPS_ERR_STATE;
-    if (!aligned(grad_pyramid, 16) || !aligned(grad, 16)) return TRIPS_ERR_ALIGN;
+    if (!aligned(grad_pyramid, 16) || !aligned(grad, 16) || !aligned(grad_camera, 4)) return TRIPS_ERR_ALIGN;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     Params P = make_params(p, ws);
     int rc;
     {
         StageScope sc(p, 4, st);
-        TRIPS_FC_SWITCH(p->FC, (k_backward<kFC><<<p->T, kTilePix, 0, st>>>(P, grad_pyramid, grad)));
+        if (grad_camera) {
+            TRIPS_FC_SWITCH(p->FC, (k_backward<kFC, true><<<p->T, kTilePix, 0, st>>>(P, grad_pyramid, grad,
+                                                                                       grad_camera)));
+        } else {
+            TRIPS_FC_SWITCH(p->FC, (k_backward<kFC, false><<<p->T, kTilePix, 0, st>>>(P, grad_pyramid, grad,
+                                                                                        nullptr)));
+        }
         if ((rc = check_launch())) return rc;
     }
     return TRIPS_OK;

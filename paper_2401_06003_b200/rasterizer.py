@@ -76,14 +76,18 @@ class Rasterizer:
                 "trips_splat_forward")
         return out
 
-    def backward(self, grad_pyramid, grad=None):
-        """Accumulates into grad [n, G] (packed rows: dx, dy, dz, ds_w, dalpha, dtau[F], pad)."""
+    def backward(self, grad_pyramid, grad=None, grad_camera=None):
+        """Accumulates into grad [n, G] (packed rows: dx, dy, dz, ds_w, dalpha, dtau[F], pad) and,
+        if given, into grad_camera [17] (dR row-major, dt, dfx, dfy, dcx, dcy, df)."""
         if grad is None:
             grad = torch.zeros(self.n, self.G, dtype=torch.float32, device=self.device)
         if not grad_pyramid.is_contiguous() or grad_pyramid.numel() != self.pyramid_floats:
             raise ValueError("grad_pyramid must be contiguous with trips_pyramid_floats elements")
+        if grad_camera is not None and (grad_camera.numel() != 17 or grad_camera.dtype != torch.float32
+                                        or not grad_camera.is_contiguous()):
+            raise ValueError("grad_camera must be a contiguous float32 tensor of 17 elements")
         A.check(A.trips_splat_backward(self.plan, self.ws.data_ptr(), grad_pyramid.data_ptr(), grad.data_ptr(),
-                                       _stream_handle()), "trips_splat_backward")
+                                       _ptr(grad_camera), _stream_handle()), "trips_splat_backward")
         return grad
 
     # ---- views / introspection ------------------------------------------------------

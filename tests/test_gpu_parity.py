@@ -357,3 +357,45 @@ def test_morton_order_permutation(dev):
     sel = pixel_float_index(sc.cams[0], sc.n_layers, F1, same_pix)
     assert np.array_equal(a["pyr"][sel], b["pyr"][sel])
     del Rasterizer
+
+
+# ------------------------------------------------------------------ camera gradient (8(f) row 1)
+
+def _camera_grad_case(sc, dev, mask=None, seed=3):
+    from paper_2401_06003_b200 import Rasterizer
+    cam = sc.cams[0]
+    G = grads_for(sc, cam, seed=seed, mask=mask)
+    r = Rasterizer(cam.width, cam.height, sc.n_layers, sc.F, max_points=max(sc.n, 1), device=dev)
+    pos, sw, al, de = (T(a, dev) for a in (sc.pos, sc.sw, sc.alpha, sc.desc))
+    r.project(cam, pos, sw, al, de)
+    r.forward(save=True)
+    gcam = torch.zeros(17, device=dev)
+    grad = r.backward(T(G, dev), grad_camera=gcam)
+    grad_nocam = r.backward(T(G, dev))                  # the CAM=false kernel gives the same point grads
+    torch.cuda.synchronize()
+    gc = np.zeros(17)
+    gcm = np.zeros(17)
+    g, gm = oracle.backward(cam, sc.n_layers, sc.pos, sc.sw, sc.alpha, sc.desc, G, mask=mask, grad_cam=gc,
+                            grad_cam_mag=gcm)
+    got = gcam.cpu().numpy().astype(np.float64)
+    err = np.abs(got - gc)
+    bad = err > GRAD_TOL * gcm + 1e-30
+    assert not bad.any(), [(oracle.CAMERA_GRAD_NAMES[k], got[k], gc[k], gcm[k]) for k in np.nonzero(bad)[0]]
+    a = grad.cpu().numpy()
+    b = grad_nocam.cpu().numpy()
+    assert np.all(np.abs(a - b) <= 1e-3 * np.abs(b) + 1e-6 * np.abs(b).max())
+
+
+def test_camera_gradient_c1(dev):
+    _camera_grad_case(scenes.c1(), dev)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_camera_gradient_random(dev, seed):
+    _camera_grad_case(scenes.tiny_scene(seed), dev, seed=seed)
+
+
+def test_camera_gradient_adversarial_and_full_size(dev):
+    _camera_grad_case(scenes.adversarial_scene(), dev)
+    sc = scenes.make_config("C3", n=1_000_000)
+    _camera_grad_case(sc, dev, mask=_sample_mask(sc.cams[0], sc.n_layers, seed=9))
