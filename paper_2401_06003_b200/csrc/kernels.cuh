@@ -29,6 +29,25 @@ constexpr int kPairsPerThread = kChunk / kTilePix;
 constexpr int kBatch = 4;                   // record gathers issued together (memory-level parallelism)
 constexpr int kBlendBatch = TRIPS_BLEND_BATCH;  // same in k_raster's blend (register budget: 3 CTAs/SM)
 
+// Experiment builds only (-DTRIPS_PHASE_CLOCK): per-phase clock64 accumulation of k_raster
+// (thread 0 of each CTA, after a barrier), read with trips_debug_phase_clocks().
+#ifdef TRIPS_PHASE_CLOCK
+__device__ unsigned long long g_pclk[8];
+#define TRIPS_PCLK_START long long _pc_t = clock64()
+#define TRIPS_PCLK(k)                                                                            \
+    do {                                                                                         \
+        __syncthreads();                                                                         \
+        if (threadIdx.x == 0) {                                                                  \
+            const long long _n = clock64();                                                      \
+            atomicAdd(&g_pclk[k], (unsigned long long)(_n - _pc_t));                             \
+            _pc_t = _n;                                                                          \
+        }                                                                                        \
+    } while (0)
+#else
+#define TRIPS_PCLK_START (void)0
+#define TRIPS_PCLK(k) (void)0
+#endif
+
 __device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d)
 {
 #ifdef TRIPS_EXP_NORED      // experiment builds only (tools/variants.sh): measure without the reductions
@@ -135,10 +154,16 @@ __device__ __forceinline__ TileCoord tile_coord(const Params& P, int t)
 
 // --------------------------------------------------------------------------- K4 raster
 
+// Dynamic shared memory of k_raster: the per-chunk fragment keys.  (Reusing it after the last
+// chunk to stage the kept records for the blend with one cp.async wave was measured slower:
+// 64 KB per CTA shrinks L1 -- profiles/r01_v2.md.)
+__host__ __device__ constexpr int raster_dyn_smem() { return kChunk * 32; }
+
 template <int FC>
 __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P, float* __restrict__ pyramid, int save)
 {
-    __shared__ uint64_t s_keys[kChunk * 4];
+    extern __shared__ __align__(16) uint64_t s_dyn[];
+    uint64_t* s_keys = s_dyn;                        // [kChunk * 4] fragment keys of a chunk
     __shared__ uint32_t s_cnt[kTilePix];
     __shared__ uint32_t s_base[kTilePix];
     __shared__ uint32_t s_rej[kTilePix];             // fragments rejected by the threshold
@@ -161,6 +186,7 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
     uint32_t total = 0;
 
     s_thr[tid] = kKeyMax;
+    TRIPS_PCLK_START;
     // Chunks interleave the bin (chunk ch takes positions ch, ch + nch, ...): a pixel's
     // fragments then spread evenly over the chunks whatever the point order, which balances
     // the per-pixel merge work inside a chunk and lets the 16th-key threshold of earlier
@@ -205,11 +231,13 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
             }
         }
         __syncthreads();
+        TRIPS_PCLK(0);
         uint32_t chunk_total;
         const uint32_t my_cnt = s_cnt[tid];
         const uint32_t my_base = block_excl_scan(my_cnt, s_warp, &chunk_total);
         s_base[tid] = my_base;
         __syncthreads();
+        TRIPS_PCLK(1);
         // phase B: counting-sort scatter by pixel (keys re-read from L1 instead of being held
         // in registers across the scan)
 #pragma unroll
@@ -223,9 +251,36 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
             }
         }
         __syncthreads();
+        TRIPS_PCLK(2);
         // phase C: merge this pixel's new fragments into its running top-16.  Network sizes are
         // chosen per warp (8 when no lane of the warp has more than 8 keys left in the group).
         const uint32_t wcnt = __reduce_max_sync(0xffffffffu, my_cnt);
+#ifdef TRIPS_GROUP8
+        // 8-key groups only: fewer live registers (4 CTAs/SM), slightly more comparators
+        for (uint32_t g = 0; g < wcnt; g += 8) {
+            const uint32_t rem = my_cnt > g ? my_cnt - g : 0u;
+            const bool first = __all_sync(0xffffffffu, total == 0 && g == 0);
+            uint64_t t8[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) t8[j] = ((uint32_t)j < rem) ? s_keys[my_base + g + j] : kKeyMax;
+            cswap(t8[0], t8[1]); cswap(t8[2], t8[3]); cswap(t8[0], t8[2]); cswap(t8[1], t8[3]); cswap(t8[1], t8[2]);
+            cswap(t8[4], t8[5]); cswap(t8[6], t8[7]); cswap(t8[4], t8[6]); cswap(t8[5], t8[7]); cswap(t8[5], t8[6]);
+            cswap(t8[0], t8[4]); cswap(t8[2], t8[6]); cswap(t8[2], t8[4]); cswap(t8[1], t8[5]); cswap(t8[3], t8[7]);
+            cswap(t8[3], t8[5]); cswap(t8[1], t8[2]); cswap(t8[3], t8[4]); cswap(t8[5], t8[6]);
+            if (first) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) r[j] = t8[j];
+            } else {
+#pragma unroll
+                for (int j = 8; j < 16; ++j) r[j] = r[j] < t8[15 - j] ? r[j] : t8[15 - j];
+#pragma unroll
+                for (int d = 8; d > 0; d >>= 1)
+#pragma unroll
+                    for (int i = 0; i < 16; ++i)
+                        if ((i & d) == 0) cswap(r[i], r[i + d]);
+            }
+        }
+#else
         for (uint32_t g = 0; g < wcnt; g += 16) {
             const uint32_t rem = my_cnt > g ? my_cnt - g : 0u;
             const bool first = __all_sync(0xffffffffu, total == 0 && g == 0);
@@ -252,9 +307,11 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
                 }
             }
         }
+#endif
         total += my_cnt + s_rej[tid];
         s_thr[tid] = r[15];                          // 16th smallest key so far (MAX if < 16)
         __syncthreads();
+        TRIPS_PCLK(3);
     }
 
     // phase D: front-to-back blend of the kept list (Eqs. 5-6; alpha_m := gamma_m, Q10).
@@ -263,7 +320,9 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
     const int K = valid ? (int)min(total, (uint32_t)kCap) : 0;
     uint32_t ktot;
     const uint32_t koff = block_excl_scan((uint32_t)K, s_warp, &ktot);
+    TRIPS_PCLK(4);
     const size_t kidx = (size_t)P.tile_kbase[t] + koff;
+    constexpr int kR4 = 1 + FC / 4;                  // float4s per point record
     float C[FC];
 #pragma unroll
     for (int c = 0; c < FC; ++c) C[c] = 0.f;
@@ -278,7 +337,7 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
             const uint32_t ii = (uint32_t)(mm < K ? r[mm] : r[0]);
             const float4* rp = reinterpret_cast<const float4*>(P.rec + (size_t)ii * P.RS);
 #pragma unroll
-            for (int c4 = 0; c4 <= FC / 4; ++c4) rb[u][c4] = __ldg(rp + c4);
+            for (int c4 = 0; c4 < kR4; ++c4) rb[u][c4] = __ldg(rp + c4);
         }
 #pragma unroll
         for (int u = 0; u < kBlendBatch; ++u) {
@@ -308,6 +367,7 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
             if (c < P.F) out[c * plane] = C[c];
         out[P.F * plane] = A;
     }
+    TRIPS_PCLK(5);
 
     // phase E: store the sorted kept lists and per-pixel metadata
     P.pix_cnt[(size_t)t * kTilePix + tid] = valid ? total : 0u;
@@ -318,6 +378,7 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
         for (int mm = 0; mm < kCap; ++mm)
             if (mm < K) kp[mm] = r[mm];
     }
+    TRIPS_PCLK(6);
 }
 
 // --------------------------------------------------------------------------- K5 backward

@@ -315,7 +315,14 @@ int trips_splat_forward(trips_plan* p, void* ws, float* pyramid, uint32_t flags,
     {
         StageScope sc(p, 3, st);
         const int save = (flags & TRIPS_FWD_SAVE_FOR_BACKWARD) ? 1 : 0;
-        TRIPS_FC_SWITCH(p->FC, (k_raster<kFC><<<p->T, kTilePix, 0, st>>>(P, pyramid, save)));
+        const size_t rsm = (size_t)raster_dyn_smem();
+        static bool rattr[9] = {};
+        if (!rattr[p->FC / 4]) {
+            TRIPS_FC_SWITCH(p->FC, (cudaFuncSetAttribute(k_raster<kFC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                         (int)rsm)));
+            rattr[p->FC / 4] = true;
+        }
+        TRIPS_FC_SWITCH(p->FC, (k_raster<kFC><<<p->T, kTilePix, rsm, st>>>(P, pyramid, save)));
         if ((rc = check_launch())) return rc;
     }
     p->stage = (flags & TRIPS_FWD_SAVE_FOR_BACKWARD) ? 2 : 3;
@@ -418,6 +425,19 @@ int trips_read_stage_ms(trips_plan* p, double* ms, int64_t* launches, int32_t ma
 }
 
 int64_t trips_launch_count(void) { return (int64_t)g_launches.load(); }
+
+#ifdef TRIPS_PHASE_CLOCK
+// experiment builds only: k_raster per-phase clocks (see kernels.cuh)
+int trips_debug_phase_clocks(unsigned long long* host8, int reset)
+{
+    if (cudaMemcpyFromSymbol(host8, g_pclk, 8 * sizeof(unsigned long long)) != cudaSuccess) return TRIPS_ERR_CUDA;
+    if (reset) {
+        unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        cudaMemcpyToSymbol(g_pclk, z, sizeof(z));
+    }
+    return TRIPS_OK;
+}
+#endif
 
 size_t trips_morton_workspace_bytes(int64_t n)
 {
