@@ -94,17 +94,22 @@ class ClockSampler:
 # ------------------------------------------------------------------ algorithmic bytes
 
 def alg_bytes(st, n, F, P):
-    """Compulsory DRAM bytes per view and kernel.
-    st: trips stats of the view (n_visible, n_pairs, n_frag, n_kept)."""
-    nv, npairs, nk = st["n_visible"], st["n_pairs"], st["n_kept"]
-    G = 8 + 4 * ((F + 3) // 4)
-    rec = 16 + 4 * F                                           # screen record (x, y, s, alpha, tau)
+    """Algorithmic bytes per view (SURVEY.md 8(d) per-unit figures), attributed to the kernel
+    whose stage consumes / produces them:
+      forward : 16 N (pos, s_w) | (4+4F) N_vis (alpha, tau) | 16 N_frag ((z, i) lists written
+                and read) | 8 P (counts, offsets) | 4 (F+1) P (pyramid) | 4 N_kept (saved list)
+      backward: 4 (F+1) P (grad pyramid) | 4 N_kept + 4 P (saved list, offsets) |
+                (20+4F) N_vis (record, alpha, tau) | 2 * 4 (5+F) N_vis (gradient accumulation) |
+                4 (5+F) N (world gradients)
+    st: trips stats of the view (n_visible, n_frag, n_kept)."""
+    nv, nf, nk = st["n_visible"], st["n_frag"], st["n_kept"]
     k = {}
-    k["count"] = 16 * n                                        # read pos, s_w
-    k["emit"] = (16 + 4 + 4 * F) * n + rec * n + 12 * npairs   # read inputs; write record + pairs
-    k["sort"] = 2 * (12 + 12 + 4) * npairs                     # 2 radix passes: histogram + move
-    k["raster"] = 12 * npairs + rec * nv + 4 * (F + 1) * P + 8 * nk + 8 * P
-    k["backward"] = 8 * nk + 4 * P + 4 * (F + 1) * P + rec * nv + 2 * 4 * G * nv
+    k["count"] = 16 * n
+    k["emit"] = 8 * nf
+    k["raster"] = (4 + 4 * F) * nv + 8 * nf + 8 * P + 4 * (F + 1) * P + 4 * nk
+    k["backward"] = (4 * (F + 1) * P + 4 * nk + 4 * P + (20 + 4 * F) * nv + 8 * (5 + F) * nv
+                     + 4 * (5 + F) * n)
+    k["sort"] = 0
     return k
 
 
@@ -267,6 +272,33 @@ def run_cuda(args, rank, world, local_rank):
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms_max = float(ms_t.item())
 
+    # ---- side measurement: backward with the camera gradient
+    gcam = torch.zeros(17, dtype=torch.float32, device=dev)
+    cam_ms = {}
+    for with_cam in (False, True):
+        rast.stage_ms(reset=True)
+        rast.set_profiling(True)
+        for v in my_views[:8]:
+            rast.project(sc.cams[v], d["pos"], d["sw"], d["alpha"], d["desc"])
+            rast.forward(save=True)
+            rast.backward(Gp, grad, grad_camera=gcam if with_cam else None)
+        torch.cuda.synchronize()
+        st_ = rast.stage_ms(reset=True)
+        rast.set_profiling(False)
+        cam_ms["with_camera_grad" if with_cam else "without"] = st_["backward"][0] / max(st_["backward"][1], 1)
+
+    # ---- side measurement: 4-NN point-size initialisation of the cloud
+    from paper_2401_06003_b200 import knn_sizes
+    knn_sizes(d["pos"])
+    torch.cuda.synchronize()
+    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    k0.record(stream)
+    for _ in range(3):
+        knn_sizes(d["pos"])
+    k1.record(stream)
+    torch.cuda.synchronize()
+    knn_ms = k0.elapsed_time(k1) / 3
+
     # ---- end to end through the public API: pinned host inputs in, gradients out
     out_host = torch.empty(n, rast.G, dtype=torch.float32).pin_memory()
     h2d = sum(v.numel() * v.element_size() for v in host.values())
@@ -321,6 +353,7 @@ def run_cuda(args, rank, world, local_rank):
             "points_per_s": N_VIEWS * n / (step_ms * 1e-3),
             "fragments_per_s": sum(s["n_frag"] for s in view_stats) * world / (step_ms * 1e-3),
             "alg_GBps_step": step_bytes * world / (step_ms * 1e-3) / 1e9,
+            "alg_frac_step": step_bytes * world / (step_ms * 1e-3) / 1e9 / peak,
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "alg_bytes_per_launch": dom_bytes, "launch_ms": dom_launch_ms},
@@ -335,6 +368,17 @@ def run_cuda(args, rank, world, local_rank):
             line["clocks"] = clk
         if random_order is not None:
             line["random_point_order"] = random_order
+        line["backward_ms_per_view"] = cam_ms
+        knn = {"ms": knn_ms, "points_per_s": n / (knn_ms * 1e-3)}
+        if world == 1 and not args.no_cpu_baseline:
+            from oracle import oracle as _o
+            qs = np.random.default_rng(0).choice(n, 64, replace=False)
+            t0 = time.perf_counter()
+            _o.knn4(sc.pos, queries=qs)
+            dt = time.perf_counter() - t0
+            knn["cpu_baseline"] = {"points_per_s": len(qs) / dt, "cores": 1, "kind": "oracle",
+                                   "sample": "64 query points, brute force over all 8M points"}
+        line["knn4_size_init"] = knn
         if world == 1 and not args.no_cpu_baseline:
             from oracle import oracle as _o  # noqa: F401  (cpu_baseline leg only)
             t = [oracle_sample(sc, sc.cams[k], phase=k + 3) for k in range(2)]

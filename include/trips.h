@@ -190,6 +190,19 @@ int trips_read_stage_ms(trips_plan* plan, double* ms, int64_t* launches, int32_t
 size_t trips_morton_workspace_bytes(int64_t n);
 int trips_morton_order(void* ws, int64_t n, const float* pos, int32_t* perm_out, void* stream);
 
+/* Point-size initialisation ("Point sizes are initialized with the average
+ * distance to the four nearest neighbor"; reading Q25): size_out[i] = mean Euclidean distance
+ * from point i to its K = min(4, #finite points - 1) nearest other finite points, neighbours
+ * ordered by (squared distance, index) with d^2 = ((dx^2 + dy^2) + dz^2) in fp32 and the mean
+ * (((d1 + d2) + d3) + d4) / K in fp32 (bit-identical to a brute-force evaluation); 0 for
+ * non-finite points.  One-time initialisation, not part of the per-view path.
+ *   ws       device scratch of trips_knn_workspace_bytes(n) bytes, 256-B aligned
+ *   pos      float[n][3] device;  size_out float[n] device;  nbr_out nullable int32[n][4]
+ *            (neighbour indices in order, -1 padded)
+ * Errors: TRIPS_ERR_ARG, TRIPS_ERR_ALIGN, TRIPS_ERR_CAPACITY (n >= 2^30), TRIPS_ERR_CUDA. */
+size_t trips_knn_workspace_bytes(int64_t n);
+int trips_knn_sizes(void* ws, int64_t n, const float* pos, float* size_out, int32_t* nbr_out, void* stream);
+
 /* Total kernel launches issued by this library in this process. */
 int64_t trips_launch_count(void);
 

@@ -40,8 +40,24 @@ def _lib(real: str):
         lib.oracle_backward.restype = C.c_int
         lib.oracle_backward.argtypes = [C.POINTER(_Camera), C.c_int, C.c_int, C.c_int64, vp, vp, vp, vp,
                                         vp, vp, vp, vp, vp, vp]
+        lib.oracle_knn4.restype = C.c_int
+        lib.oracle_knn4.argtypes = [C.c_int64, vp, C.c_int64, vp, vp, vp]
         _LIBS[real] = lib
     return _LIBS[real]
+
+
+def knn4(pos, queries=None):
+    """4-NN size init (reading Q25): returns (size float32 [q], nbr int32 [q,4])
+    for the query indices (all points if None), brute force over all points."""
+    pos = _f32(pos, (-1, 3))
+    n = pos.shape[0]
+    q = None if queries is None else np.ascontiguousarray(queries, dtype=np.int64)
+    nq = n if q is None else q.shape[0]
+    size = np.zeros(nq, np.float32)
+    nbr = np.full((nq, 4), -1, np.int32)
+    rc = _lib("float").oracle_knn4(n, _ptr(pos), nq, _ptr(q), _ptr(size), _ptr(nbr))
+    assert rc == 0, rc
+    return size, nbr
 
 
 def camera_struct(cam) -> _Camera:

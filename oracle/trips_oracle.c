@@ -554,3 +554,50 @@ int oracle_backward(const oracle_camera* cam, int n_layers, int F, int64_t n, co
     free_scene(&S);
     return 0;
 }
+
+/* ---------------------------------------------------------------- 4-NN size init */
+
+/* Point-size initialisation, PAPER.md:302 ("Point sizes are initialized with the average
+ * distance to the four nearest neighbor"), SURVEY.md 8(f) row 4.  Reading Q25:
+ * for point i the K = min(4, #finite - 1) other finite points j with the smallest
+ * (d2_ij, j), d2 = ((xj-xi)^2 + (yj-yi)^2) + (zj-zi)^2 evaluated in fp32 with every operation
+ * rounded; size_i = (((sqrt d1 + sqrt d2) + sqrt d3) + sqrt d4) / K in fp32 (0 if K = 0 or
+ * the point is not finite).  Brute force over all points: O(n) per query.
+ *   queries  nullable: query indices (nq of them); NULL = all n points (nq ignored)
+ *   size_out [nq] float, nbr_out nullable [nq][4] int32 (-1 padded), in query order */
+static int finite3(const float* p) { return isfinite(p[0]) && isfinite(p[1]) && isfinite(p[2]); }
+
+int oracle_knn4(int64_t n, const float* pos, int64_t nq, const int64_t* queries, float* size_out, int32_t* nbr_out)
+{
+    if (n < 0 || !pos || !size_out) return -1;
+    if (!queries) nq = n;
+    for (int64_t q = 0; q < nq; ++q) {
+        int64_t i = queries ? queries[q] : q;
+        float bd[4];
+        int64_t bj[4];
+        int nb = 0;
+        const float* pi = pos + 3 * i;
+        if (finite3(pi)) {
+            for (int64_t j = 0; j < n; ++j) {
+                if (j == i) continue;
+                const float* pj = pos + 3 * j;
+                if (!finite3(pj)) continue;
+                float dx = pj[0] - pi[0], dy = pj[1] - pi[1], dz = pj[2] - pi[2];
+                float xx = dx * dx, yy = dy * dy, zz = dz * dz;
+                float d2 = xx + yy;
+                d2 = d2 + zz;
+                /* insert (d2, j) into the ascending top-4 (j increases, so ties keep order) */
+                if (nb == 4 && !(d2 < bd[3])) continue;
+                int k = nb < 4 ? nb++ : 3;
+                while (k > 0 && d2 < bd[k - 1]) { bd[k] = bd[k - 1]; bj[k] = bj[k - 1]; --k; }
+                bd[k] = d2; bj[k] = j;
+            }
+        }
+        float s = 0.0f;
+        for (int k = 0; k < nb; ++k) s = s + sqrtf(bd[k]);
+        size_out[q] = nb ? s / (float)nb : 0.0f;
+        if (nbr_out)
+            for (int k = 0; k < 4; ++k) nbr_out[4 * q + k] = k < nb ? (int32_t)bj[k] : -1;
+    }
+    return 0;
+}

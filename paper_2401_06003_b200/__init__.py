@@ -10,6 +10,6 @@ sm_100a in csrc/).  This package is its thin Python binding:
 There is no CPU fallback: importing the binding loads libtrips.so or raises.
 """
 from . import _abi  # noqa: F401
-from .rasterizer import Rasterizer, morton_order, render  # noqa: F401
+from .rasterizer import Rasterizer, knn_sizes, morton_order, render  # noqa: F401
 
-__all__ = ["Rasterizer", "render", "morton_order"]
+__all__ = ["Rasterizer", "render", "morton_order", "knn_sizes"]

@@ -70,6 +70,8 @@ SIGNATURES = [
     ("trips_read_stage_ms", C.c_int, [_VP, C.POINTER(C.c_double), C.POINTER(C.c_int64), C.c_int32, C.c_int32]),
     ("trips_morton_workspace_bytes", C.c_size_t, [C.c_int64]),
     ("trips_morton_order", C.c_int, [_VP, C.c_int64, _VP, _VP, _VP]),
+    ("trips_knn_workspace_bytes", C.c_size_t, [C.c_int64]),
+    ("trips_knn_sizes", C.c_int, [_VP, C.c_int64, _VP, _VP, _VP, _VP]),
     ("trips_launch_count", C.c_int64, []),
     ("trips_status_string", C.c_char_p, [C.c_int]),
 ]
@@ -191,6 +193,14 @@ def trips_morton_workspace_bytes(n):
 
 def trips_morton_order(ws, n, pos, perm_out, stream=None):
     return lib().trips_morton_order(ws, n, pos, perm_out, stream)
+
+
+def trips_knn_workspace_bytes(n):
+    return int(lib().trips_knn_workspace_bytes(n))
+
+
+def trips_knn_sizes(ws, n, pos, size_out, nbr_out=None, stream=None):
+    return lib().trips_knn_sizes(ws, n, pos, size_out, nbr_out, stream)
 
 
 def trips_launch_count():

@@ -11,6 +11,7 @@
 
 #include "../../include/trips.h"
 #include "kernels.cuh"
+#include "knn.cuh"
 #include "morton.cuh"
 
 using namespace trips;
@@ -425,6 +426,58 @@ int trips_read_stage_ms(trips_plan* p, double* ms, int64_t* launches, int32_t ma
 }
 
 int64_t trips_launch_count(void) { return (int64_t)g_launches.load(); }
+
+size_t trips_knn_workspace_bytes(int64_t n)
+{
+    if (n < 0) return 0;
+    const size_t N = (size_t)(n > 0 ? n : 1), cap = N + 1;
+    return align256(6 * 4) + align256(sizeof(KnnGrid)) + align256(N * 4) + align256((cap + 1) * 4) +
+           align256(cap * 4) + align256(((cap + 1023) / 1024 + 1) * 4) + align256(N * 16);
+}
+
+int trips_knn_sizes(void* ws, int64_t n, const float* pos, float* size_out, int32_t* nbr_out, void* stream)
+{
+    if (!ws || n < 0 || (n > 0 && (!pos || !size_out))) return TRIPS_ERR_ARG;
+    if (n >= (int64_t(1) << 30)) return TRIPS_ERR_CAPACITY;
+    if (!aligned(ws, 256) || !aligned(pos, 4) || !aligned(size_out, 4) || !aligned(nbr_out, 4)) return TRIPS_ERR_ALIGN;
+    if (n == 0) return TRIPS_OK;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t N = (size_t)n, cap = N + 1;
+    KnnWs W;
+    W.n = (int)n;
+    W.cap = (int)cap;
+    char* b = static_cast<char*>(ws);
+    size_t o = 0;
+    W.bbox = reinterpret_cast<uint32_t*>(b + o);    o += align256(6 * 4);
+    W.grid = reinterpret_cast<KnnGrid*>(b + o);     o += align256(sizeof(KnnGrid));
+    W.cell_of = reinterpret_cast<uint32_t*>(b + o); o += align256(N * 4);
+    W.cnt = reinterpret_cast<uint32_t*>(b + o);     o += align256((cap + 1) * 4);
+    W.cur = reinterpret_cast<uint32_t*>(b + o);     o += align256(cap * 4);
+    W.bsum = reinterpret_cast<uint32_t*>(b + o);    o += align256(((cap + 1023) / 1024 + 1) * 4);
+    W.pts = reinterpret_cast<float4*>(b + o);
+    int rc = cuda_status(cudaMemsetAsync(W.bbox, 0xff, 3 * 4, st));
+    if (rc) return rc;
+    if ((rc = cuda_status(cudaMemsetAsync(W.bbox + 3, 0, 3 * 4, st)))) return rc;
+    if ((rc = cuda_status(cudaMemsetAsync(W.cnt, 0, (cap + 1) * 4, st)))) return rc;
+    const int pb = (W.n + 255) / 256;
+    k_knn_bbox<<<std::min(pb, 148 * 8), 256, 0, st>>>(W, pos);
+    if ((rc = check_launch())) return rc;
+    k_knn_setup<<<1, 1, 0, st>>>(W);
+    if ((rc = check_launch())) return rc;
+    k_knn_count<<<pb, 256, 0, st>>>(W, pos);
+    if ((rc = check_launch())) return rc;
+    const int sb = (int)((cap + 1023) / 1024);       // upper bound of the scan blocks
+    k_knn_scan_a<<<sb, 1024, 0, st>>>(W);
+    if ((rc = check_launch())) return rc;
+    k_knn_scan_b<<<1, 1024, 0, st>>>(W);
+    if ((rc = check_launch())) return rc;
+    k_knn_scan_c<<<sb, 1024, 0, st>>>(W);
+    if ((rc = check_launch())) return rc;
+    k_knn_fill<<<pb, 256, 0, st>>>(W, pos);
+    if ((rc = check_launch())) return rc;
+    k_knn_query<<<pb, 256, 0, st>>>(W, pos, size_out, nbr_out);
+    return check_launch();
+}
 
 #ifdef TRIPS_PHASE_CLOCK
 // experiment builds only: k_raster per-phase clocks (see kernels.cuh)

@@ -159,5 +159,18 @@ def morton_order(pos):
     return perm.long()
 
 
+def knn_sizes(pos, return_neighbors=False):
+    """Initial world sizes s_w = mean distance to the 4 nearest neighbours,
+    computed on the GPU (trips_knn_sizes).  Returns size [n] (and neighbours [n, 4])."""
+    _check_input("pos", pos, (3,))
+    n = pos.shape[0]
+    ws = torch.empty(max(A.trips_knn_workspace_bytes(n), 256), dtype=torch.uint8, device=pos.device)
+    size = torch.empty(n, dtype=torch.float32, device=pos.device)
+    nbr = torch.empty(n, 4, dtype=torch.int32, device=pos.device) if return_neighbors else None
+    A.check(A.trips_knn_sizes(ws.data_ptr(), n, pos.data_ptr(), size.data_ptr(), _ptr(nbr), _stream_handle()),
+            "trips_knn_sizes")
+    return (size, nbr) if return_neighbors else size
+
+
 def render(rast, cam, pos, world_size, opacity, desc):
     return rast.render(cam, pos, world_size, opacity, desc)
