@@ -59,6 +59,10 @@ typedef struct {
 typedef struct {
     int32_t num_layers;        /* n in [1, 16]  (paper studies 3..8) */
     int32_t num_features;      /* F in [1, 32]  (paper uses 4..8) */
+    float t_min;               /* 0 = the exact definition.  In [0, 1): variant with early
+                                  termination -- a pixel's kept list ends with the fragment
+                                  after which the fp32 transmittance T = prod (1 - gamma) drops
+                                  below t_min (reading Q17) */
 } trips_config;
 
 typedef struct trips_plan trips_plan;   /* opaque, host memory, owned by the library */

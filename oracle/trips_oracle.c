@@ -322,6 +322,30 @@ static fw_t frag_weights(const scene_t* S, const frag_t* f)
     return w;
 }
 
+/* ---------------------------------------------------------------- T_min variant */
+
+/* SURVEY.md 8(f) row 3 / reading Q17: with t_min > 0 (a variant, not the paper's definition)
+ * a pixel's kept list ends with the fragment after which the transmittance drops below
+ * t_min.  The cut is an integer decision taken in fp32 (T = T * (1 - gamma), each op rounded)
+ * so that both implementations take it identically.  t_min = 0 (default) never cuts. */
+static float g_t_min = 0.0f;
+
+void oracle_set_t_min(float t) { g_t_min = t; }
+
+static fw_t frag_weights(const scene_t* S, const frag_t* f);
+
+static int64_t tmin_cut(const scene_t* S, int64_t b, int64_t K)
+{
+    if (!(g_t_min > 0.0f)) return K;
+    float T = 1.0f;
+    for (int64_t m = 0; m < K; ++m) {
+        const float g = (float)frag_weights(S, &S->frags[b + m]).gamma;
+        T = T * (1.0f - g);
+        if (T < g_t_min) return m + 1;
+    }
+    return K;
+}
+
 /* ---------------------------------------------------------------- forward */
 
 /* Forward rasterization.
@@ -362,6 +386,7 @@ int oracle_forward(const oracle_camera* cam, int n_layers, int F, int64_t n, con
             if (len > ORACLE_CAP) st.n_trunc_pixels++;
             if (len > st.max_list) st.max_list = len;
             st.n_kept += K;
+            K = tmin_cut(&S, b, K);
             double T = 1.0, A = 0.0, C[64], M[64];
             for (int c = 0; c < F; ++c) { C[c] = 0.0; M[c] = 0.0; }
             for (int64_t m = 0; m < K; ++m) {                /* Eqs. (5)-(6), alpha_m = gamma (Q10) */
@@ -432,6 +457,7 @@ int oracle_backward(const oracle_camera* cam, int n_layers, int F, int64_t n, co
             int64_t p = poff + q;
             int64_t b = S.seg[p], e = S.seg[p + 1];
             int64_t K = (e - b) < ORACLE_CAP ? (e - b) : ORACLE_CAP;
+            K = tmin_cut(&S, b, K);
             if (K == 0) continue;
             double gC[64], gA = (double)grad_pyramid[foff + F * plane + q];
             for (int c = 0; c < F; ++c) gC[c] = (double)grad_pyramid[foff + c * plane + q];

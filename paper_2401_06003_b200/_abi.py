@@ -32,7 +32,7 @@ class trips_camera(C.Structure):
 
 
 class trips_config(C.Structure):
-    _fields_ = [("num_layers", C.c_int32), ("num_features", C.c_int32)]
+    _fields_ = [("num_layers", C.c_int32), ("num_features", C.c_int32), ("t_min", C.c_float)]
 
 
 class trips_stats(C.Structure):
@@ -105,8 +105,8 @@ def check(status, where):
 
 # ---- same names as include/trips.h -------------------------------------------------
 
-def trips_plan_create(num_layers, num_features, width, height, max_points):
-    cfg = trips_config(num_layers, num_features)
+def trips_plan_create(num_layers, num_features, width, height, max_points, t_min=0.0):
+    cfg = trips_config(num_layers, num_features, t_min)
     out = _VP()
     check(lib().trips_plan_create(C.byref(cfg), width, height, max_points, C.byref(out)), "trips_plan_create")
     return out.value

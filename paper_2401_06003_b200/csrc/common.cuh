@@ -38,7 +38,7 @@ struct Cam {
 struct Params {
     int32_t n, F, FC, RS, G;          // F features, FC = round_up(F,4), RS = 4 + FC, G = 8 + FC
     int32_t n_layers, T;              // layers, total tiles
-    int32_t pad0;
+    float t_min;                      // T_min blend variant (0 = the exact definition)
     LayerGeom L[kMaxLayers];
     Cam cam;
     // inputs (caller)

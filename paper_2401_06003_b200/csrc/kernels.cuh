@@ -327,9 +327,12 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
 #pragma unroll
     for (int c = 0; c < FC; ++c) C[c] = 0.f;
     float A = 0.f, T = 1.f;
+    // T_min variant (0 = the exact definition): the kept list ends with
+    // the fragment after which the fp32 transmittance drops below t_min
+    int Keff = K;
 #pragma unroll
     for (int b = 0; b < kCap / kBlendBatch; ++b) {
-        if (b * kBlendBatch >= K || (!save && T == 0.f)) break;
+        if (b * kBlendBatch >= Keff || (!save && T == 0.f)) break;
         float4 rb[kBlendBatch][1 + FC / 4];
 #pragma unroll
         for (int u = 0; u < kBlendBatch; ++u) {
@@ -342,7 +345,7 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
 #pragma unroll
         for (int u = 0; u < kBlendBatch; ++u) {
             const int mm = b * kBlendBatch + u;
-            if (mm < K) {
+            if (mm < Keff) {
                 const FragW w = frag_weights(rb[u][0], tc.l, P.n_layers, px, py);
                 const float tg = T * w.gamma;
 #pragma unroll
@@ -354,8 +357,9 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
                     C[4 * c4 + 3] = fmaf(tg, tau.w, C[4 * c4 + 3]);
                 }
                 A += tg;
-                T = T * (1.0f - w.gamma);
+                T = __fmul_rn(T, __fsub_rn(1.0f, w.gamma));      // pinned: decides the T_min cut
                 if (save) P.kept_gamma[kidx + mm] = w.gamma;
+                if (T < P.t_min) Keff = mm + 1;
             }
         }
     }
@@ -371,12 +375,12 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
 
     // phase E: store the sorted kept lists and per-pixel metadata
     P.pix_cnt[(size_t)t * kTilePix + tid] = valid ? total : 0u;
-    P.pix_meta[(size_t)t * kTilePix + tid] = (koff << 5) | (uint32_t)K;
+    P.pix_meta[(size_t)t * kTilePix + tid] = (koff << 5) | (uint32_t)Keff;
     if (save) {
         uint64_t* kp = P.kept + kidx;
 #pragma unroll
         for (int mm = 0; mm < kCap; ++mm)
-            if (mm < K) kp[mm] = r[mm];
+            if (mm < Keff) kp[mm] = r[mm];
     }
     TRIPS_PCLK(6);
 }

@@ -33,6 +33,7 @@ struct EventPair {
 
 struct trips_plan {
     int32_t n_layers, F, FC, RS, G, W, H, T;
+    float t_min;
     int64_t max_points, P, pyr_floats;
     LayerGeom L[kMaxLayers];
     uint64_t kcap;
@@ -143,6 +144,7 @@ Params make_params(const trips_plan* p, void* ws)
     P.n = (int32_t)p->n;
     P.F = p->F; P.FC = p->FC; P.RS = p->RS; P.G = p->G;
     P.n_layers = p->n_layers; P.T = p->T;
+    P.t_min = p->t_min;
     for (int l = 0; l < kMaxLayers; ++l) P.L[l] = p->L[l];
     P.cam = p->cam;
     char* b = static_cast<char*>(ws);
@@ -188,10 +190,12 @@ int trips_plan_create(const trips_config* cfg, int32_t width, int32_t height, in
     *out = nullptr;
     const int n = cfg->num_layers, F = cfg->num_features;
     if (n < 1 || n > kMaxLayers || F < 1 || F > 32) return TRIPS_ERR_ARG;
+    if (!(cfg->t_min >= 0.0f && cfg->t_min < 1.0f)) return TRIPS_ERR_ARG;
     if (width < 1 || height < 1 || width > 32768 || height > 32768) return TRIPS_ERR_ARG;
     if (max_points < 0 || max_points >= (int64_t(1) << 28)) return TRIPS_ERR_ARG;
     trips_plan* p = new trips_plan();
     p->n_layers = n; p->F = F; p->FC = (F + 3) & ~3; p->RS = 4 + p->FC; p->G = 8 + p->FC;
+    p->t_min = cfg->t_min;
     p->W = width; p->H = height; p->max_points = max_points;
     memset(p->L, 0, sizeof(p->L));
     int64_t pix = 0;

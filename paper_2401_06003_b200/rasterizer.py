@@ -31,13 +31,15 @@ def _check_input(name, t, shape_tail=()):
 class Rasterizer:
     """One plan + one workspace (one in-flight view).  Not thread-safe."""
 
-    def __init__(self, width, height, num_layers=4, num_features=4, max_points=1 << 20, device=None):
+    def __init__(self, width, height, num_layers=4, num_features=4, max_points=1 << 20, device=None, t_min=0.0):
         self.width, self.height = int(width), int(height)
         self.num_layers, self.F = int(num_layers), int(num_features)
         self.max_points = int(max_points)
         self.device = torch.device(device if device is not None else "cuda")
         A.lib()
-        self.plan = A.trips_plan_create(self.num_layers, self.F, self.width, self.height, self.max_points)
+        self.t_min = float(t_min)
+        self.plan = A.trips_plan_create(self.num_layers, self.F, self.width, self.height, self.max_points,
+                                        self.t_min)
         self.ws = torch.empty(A.trips_workspace_bytes(self.plan), dtype=torch.uint8, device=self.device)
         self.P = A.trips_num_pixels(self.plan)
         self.pyramid_floats = A.trips_pyramid_floats(self.plan)

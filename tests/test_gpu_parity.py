@@ -31,10 +31,10 @@ def T(a, dev):
     return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
 
 
-def gpu_run(sc, dev, cam=None, G=None, save=True, export=True):
+def gpu_run(sc, dev, cam=None, G=None, save=True, export=True, t_min=0.0):
     from paper_2401_06003_b200 import Rasterizer
     cam = cam or sc.cams[0]
-    r = Rasterizer(cam.width, cam.height, sc.n_layers, sc.F, max_points=max(sc.n, 1), device=dev)
+    r = Rasterizer(cam.width, cam.height, sc.n_layers, sc.F, max_points=max(sc.n, 1), device=dev, t_min=t_min)
     pos, sw, al, de = (T(a, dev) for a in (sc.pos, sc.sw, sc.alpha, sc.desc))
     level = torch.empty(sc.n, dtype=torch.int8, device=dev)
     proj = torch.empty(sc.n, 4, dtype=torch.float32, device=dev)
@@ -384,6 +384,25 @@ def _camera_grad_case(sc, dev, mask=None, seed=3):
     a = grad.cpu().numpy()
     b = grad_nocam.cpu().numpy()
     assert np.all(np.abs(a - b) <= 1e-3 * np.abs(b) + 1e-6 * np.abs(b).max())
+
+
+@pytest.mark.parametrize("t_min", [0.05, 0.4])
+def test_tmin_variant(dev, t_min):
+    """T_min early termination -- identical cut lists (the cut is an fp32
+    decision taken the same way on both sides), features and gradients within tolerance."""
+    for sc in (scenes.c1(), scenes.tiny_scene(11, n=30000, F=4, W=40, H=24, n_layers=3)):
+        cam = sc.cams[0]
+        G = grads_for(sc, cam, seed=2)
+        got = gpu_run(sc, dev, G=G, t_min=t_min)
+        ref = oracle.forward(cam, sc.n_layers, sc.pos, sc.sw, sc.alpha, sc.desc, t_min=t_min)
+        assert np.array_equal(got["kept"], ref["kept"])
+        assert np.array_equal(got["counts"], ref["counts"])
+        err = np.abs(got["pyr"].astype(np.float64) - ref["pyramid"])
+        assert np.all(err <= FEAT_TOL * ref["mag"] + 1e-30)
+        g, gm = oracle.backward(cam, sc.n_layers, sc.pos, sc.sw, sc.alpha, sc.desc, G, t_min=t_min)
+        assert np.all(np.abs(got["grad"] - g) <= GRAD_TOL * gm + 1e-30)
+        full = oracle.forward(cam, sc.n_layers, sc.pos, sc.sw, sc.alpha, sc.desc)
+        assert (ref["kept"] >= 0).sum() < (full["kept"] >= 0).sum()          # the variant does cut
 
 
 def test_camera_gradient_c1(dev):
