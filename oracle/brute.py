@@ -71,9 +71,15 @@ def _layer_weight(s, vis, l, n_layers):
     return sel, iota
 
 
-def render(cam, n_layers, pos, sw, alpha, desc):
+def render(cam, n_layers, pos, sw, alpha, desc, coarse=0):
     """Returns (list of (F+1, H_l, W_l) float64 layers, list of (H_l, W_l) counts,
-    list of (H_l, W_l, 16) kept indices, -1 padded)."""
+    list of (H_l, W_l, 16) kept indices, -1 padded).
+
+    coarse > 0: coarse-layer inclusion (reading Q22): the list blended at
+    (l, u, v) is the union of the fragments of (l + d, u >> d, v >> d), d = 0..min(coarse,
+    n_layers - 1 - l), ordered by (z, i, d), 16 kept; counts stay the pixel's own list."""
+    if coarse:
+        return _render_coarse(cam, n_layers, pos, sw, alpha, desc, coarse)
     pos = np.asarray(pos, np.float32)
     sw = np.asarray(sw, np.float32)
     alpha = np.asarray(alpha, np.float32)
@@ -116,6 +122,81 @@ def render(cam, n_layers, pos, sw, alpha, desc):
                 for j, i in enumerate(ids):
                     g = float(gamma[j])
                     C += T * g * desc[i].astype(np.float64)
+                    A += T * g
+                    T *= 1.0 - g
+                out[:F, v, u] = C
+                out[F, v, u] = A
+        layers.append(out)
+        counts.append(cnt)
+        kepts.append(kept)
+    return layers, counts, kepts
+
+
+def _pixel_fragments(cam, n_layers, xs, ys, s, vis, alpha):
+    """Per layer, per pixel: (point ids, gamma float32) of every fragment (Eq. 3), any order."""
+    f32 = np.float32
+    idx_all = np.arange(xs.shape[0])
+    out = []
+    for l in range(n_layers):
+        Hl = -(-cam.height // (1 << l))
+        Wl = -(-cam.width // (1 << l))
+        sel, iota = _layer_weight(s, vis, l, n_layers)
+        scale = f32(2.0 ** -l)
+        with np.errstate(all="ignore"):
+            xl = xs * scale
+            yl = ys * scale
+            inb = sel & (xl >= -1) & (xl < Wl) & (yl >= -1) & (yl < Hl)
+            x0 = np.floor(np.where(inb, xl, 0)).astype(np.int64)
+            y0 = np.floor(np.where(inb, yl, 0)).astype(np.int64)
+            fx = (xl - x0.astype(f32)).astype(f32)
+            fy = (yl - y0.astype(f32)).astype(f32)
+        grid = {}
+        for v in range(Hl):
+            for u in range(Wl):
+                hx = inb & ((x0 == u) | (x0 + 1 == u)) & ((y0 == v) | (y0 + 1 == v))
+                ids = idx_all[hx]
+                wx = np.where(x0[ids] + 1 == u, fx[ids], f32(1) - fx[ids]).astype(f32)
+                wy = np.where(y0[ids] + 1 == v, fy[ids], f32(1) - fy[ids]).astype(f32)
+                beta = (wx * wy).astype(f32)
+                gamma = ((beta * iota[ids]).astype(f32) * alpha[ids]).astype(f32)
+                grid[(v, u)] = (ids, gamma)
+        out.append((Hl, Wl, grid))
+    return out
+
+
+def _render_coarse(cam, n_layers, pos, sw, alpha, desc, coarse):
+    pos = np.asarray(pos, np.float32)
+    sw = np.asarray(sw, np.float32)
+    alpha = np.asarray(alpha, np.float32)
+    desc = np.asarray(desc, np.float32)
+    n, F = desc.shape
+    xs, ys, z, s, vis = _project(cam, pos, sw)
+    frags = _pixel_fragments(cam, n_layers, xs, ys, s, vis, alpha)
+    layers, counts, kepts = [], [], []
+    for l in range(n_layers):
+        Hl, Wl, grid = frags[l]
+        D = min(coarse, n_layers - 1 - l)
+        out = np.zeros((F + 1, Hl, Wl))
+        cnt = np.zeros((Hl, Wl), np.int64)
+        kept = np.full((Hl, Wl, CAP), -1, np.int64)
+        for v in range(Hl):
+            for u in range(Wl):
+                cnt[v, u] = grid[(v, u)][0].size
+                ids, gam, dd = [], [], []
+                for d in range(D + 1):
+                    a_ids, a_gam = frags[l + d][2][(v >> d, u >> d)]
+                    ids.append(a_ids)
+                    gam.append(a_gam)
+                    dd.append(np.full(a_ids.size, d))
+                ids, gam, dd = np.concatenate(ids), np.concatenate(gam), np.concatenate(dd)
+                if ids.size == 0:
+                    continue
+                order = np.lexsort((dd, ids, z[ids]))[:CAP]      # by z, then index, then d
+                kept[v, u, :order.size] = ids[order]
+                T, C, A = 1.0, np.zeros(F), 0.0
+                for j in order:
+                    g = float(gam[j])
+                    C += T * g * desc[ids[j]].astype(np.float64)
                     A += T * g
                     T *= 1.0 - g
                 out[:F, v, u] = C

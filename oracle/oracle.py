@@ -42,6 +42,8 @@ def _lib(real: str):
                                         vp, vp, vp, vp, vp, vp]
         lib.oracle_set_t_min.restype = None
         lib.oracle_set_t_min.argtypes = [C.c_float]
+        lib.oracle_set_coarse.restype = None
+        lib.oracle_set_coarse.argtypes = [C.c_int, vp]
         lib.oracle_knn4.restype = C.c_int
         lib.oracle_knn4.argtypes = [C.c_int64, vp, C.c_int64, vp, vp, vp]
         _LIBS[real] = lib
@@ -131,14 +133,22 @@ def project(cam, n_layers, pos, sw, real="float"):
     return proj, level, iota
 
 
-def forward(cam, n_layers, pos, sw, alpha, desc, mask=None, real="float", want_kept=True, t_min=0.0):
+def forward(cam, n_layers, pos, sw, alpha, desc, mask=None, real="float", want_kept=True, t_min=0.0, coarse=0):
     """O1 forward.  Returns dict(pyramid float64 flat, mag, counts uint32 [P],
-    kept int32 [P,16], stats dict).  t_min > 0 selects the T_min variant (reading Q17)."""
+    kept int32 [P,16], kept_layer int8 [P,16] (coarse only), stats dict).  t_min > 0 selects
+    the T_min variant (reading Q17), coarse > 0 coarse-layer inclusion (reading Q22)."""
+    P = num_pixels(cam.width, cam.height, n_layers)
+    kl = np.full((P, 16), -1, dtype=np.int8) if (coarse and want_kept) else None
     _lib(real).oracle_set_t_min(float(np.float32(t_min)))
+    _lib(real).oracle_set_coarse(int(coarse), _ptr(kl))
     try:
-        return _forward(cam, n_layers, pos, sw, alpha, desc, mask, real, want_kept)
+        r = _forward(cam, n_layers, pos, sw, alpha, desc, mask, real, want_kept)
     finally:
         _lib(real).oracle_set_t_min(0.0)
+        _lib(real).oracle_set_coarse(0, None)
+    if kl is not None:
+        r["kept_layer"] = kl
+    return r
 
 
 def _forward(cam, n_layers, pos, sw, alpha, desc, mask, real, want_kept):
@@ -169,17 +179,19 @@ CAMERA_GRAD_NAMES = ("R00", "R01", "R02", "R10", "R11", "R12", "R20", "R21", "R2
 
 
 def backward(cam, n_layers, pos, sw, alpha, desc, grad_pyramid, mask=None, real="float", grad=None,
-             grad_mag=None, grad_cam=None, grad_cam_mag=None, t_min=0.0):
+             grad_mag=None, grad_cam=None, grad_cam_mag=None, t_min=0.0, coarse=0):
     """O1 backward.  Returns (grad [n, 5+F] float64, grad_mag [n, 5+F]); rows are
     (d/dx, d/dy, d/dz, d/ds_w, d/dalpha, d/dtau[F]).  If grad / grad_mag are given
     they are accumulated into (multi-view sum, reading Q21).  grad_cam / grad_cam_mag
     (float64 [17], CAMERA_GRAD_NAMES order) receive the camera gradient if given."""
     _lib(real).oracle_set_t_min(float(np.float32(t_min)))
+    _lib(real).oracle_set_coarse(int(coarse), None)
     try:
         return _backward(cam, n_layers, pos, sw, alpha, desc, grad_pyramid, mask, real, grad, grad_mag, grad_cam,
                          grad_cam_mag)
     finally:
         _lib(real).oracle_set_t_min(0.0)
+        _lib(real).oracle_set_coarse(0, None)
 
 
 def _backward(cam, n_layers, pos, sw, alpha, desc, grad_pyramid, mask, real, grad, grad_mag, grad_cam,

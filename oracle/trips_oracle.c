@@ -334,16 +334,92 @@ void oracle_set_t_min(float t) { g_t_min = t; }
 
 static fw_t frag_weights(const scene_t* S, const frag_t* f);
 
-static int64_t tmin_cut(const scene_t* S, int64_t b, int64_t K)
+static int64_t tmin_cut(const scene_t* S, const frag_t* const* lst, int64_t K)
 {
     if (!(g_t_min > 0.0f)) return K;
     float T = 1.0f;
     for (int64_t m = 0; m < K; ++m) {
-        const float g = (float)frag_weights(S, &S->frags[b + m]).gamma;
+        const float g = (float)frag_weights(S, lst[m]).gamma;
         T = T * (1.0f - g);
         if (T < g_t_min) return m + 1;
     }
     return K;
+}
+
+/* ---------------------------------------------------------------- coarse-layer inclusion */
+
+/* "we include points from coarser layers during blending (in the usual
+ * way)".  Reading Q22 (a variant, off by default): with coarse = c > 0 the list
+ * blended at pyramid pixel (l, x, y) is the union of the fragment lists of its ancestors
+ * (l + d, x >> d, y >> d), d = 0 .. min(c, L - 1 - l), ordered by (z, i, d) -- depth, then
+ * point index, then the finer layer first -- of which the first 16 are kept (Sec. 3.2).  Each
+ * fragment keeps its own weight gamma (Eq. 3, evaluated in its own layer and pixel).  The
+ * per-pixel counts remain the pixel's own list length.  kept_layer (nullable, [P*16]) receives
+ * d for each kept entry (-1 padded). */
+static int g_coarse = 0;
+static int8_t* g_kept_layer = NULL;
+
+void oracle_set_coarse(int c, int8_t* kept_layer) { g_coarse = c; g_kept_layer = kept_layer; }
+
+static int list_cmp(const void* a, const void* b)
+{
+    const frag_t* x = *(const frag_t* const*)a;
+    const frag_t* y = *(const frag_t* const*)b;
+    if (x->z != y->z) return x->z < y->z ? -1 : 1;
+    if (x->i != y->i) return x->i < y->i ? -1 : 1;
+    if (x->l != y->l) return x->l < y->l ? -1 : 1;
+    return 0;
+}
+
+/* The blend list of pixel (l, x, y) (global index p): up to 16 fragment pointers in blend
+ * order.  Returns its length. */
+static int64_t blend_list(const scene_t* S, int l, int32_t x, int32_t y, int64_t p, const frag_t** out)
+{
+    const int D = g_coarse <= 0 ? 0 : (g_coarse < S->n_layers - 1 - l ? g_coarse : S->n_layers - 1 - l);
+    if (D == 0) {
+        int64_t len = S->seg[p + 1] - S->seg[p];
+        int64_t K = len < ORACLE_CAP ? len : ORACLE_CAP;    /* Sec. 3.2 */
+        for (int64_t m = 0; m < K; ++m) out[m] = &S->frags[S->seg[p] + m];
+        return K;
+    }
+    int64_t tot = 0;
+    int64_t anc[16];
+    for (int d = 0; d <= D; ++d) {
+        const int la = l + d;
+        anc[d] = layer_pixel_offset(S->n_layers, S->cam->width, S->cam->height, la)
+               + (int64_t)(y >> d) * layer_w(S->cam->width, la) + (x >> d);
+        tot += S->seg[anc[d] + 1] - S->seg[anc[d]];
+    }
+    const frag_t** all = (const frag_t**)malloc(sizeof(frag_t*) * (size_t)(tot ? tot : 1));
+    int64_t k = 0;
+    for (int d = 0; d <= D; ++d)
+        for (int64_t j = S->seg[anc[d]]; j < S->seg[anc[d] + 1]; ++j) all[k++] = &S->frags[j];
+    qsort(all, (size_t)tot, sizeof(frag_t*), list_cmp);
+    const int64_t K = tot < ORACLE_CAP ? tot : ORACLE_CAP;
+    for (int64_t m = 0; m < K; ++m) out[m] = all[m];
+    free(all);
+    return K;
+}
+
+/* With coarse inclusion a masked pixel also needs its ancestors' lists. */
+static uint8_t* coarse_mask(const oracle_camera* cam, int n_layers, const uint8_t* mask)
+{
+    if (!mask || g_coarse <= 0) return NULL;
+    const int64_t P = oracle_num_pixels(n_layers, cam->width, cam->height);
+    uint8_t* m = (uint8_t*)malloc((size_t)P);
+    memcpy(m, mask, (size_t)P);
+    for (int l = 0; l < n_layers; ++l) {
+        const int32_t Wl = layer_w(cam->width, l), Hl = layer_h(cam->height, l);
+        const int64_t off = layer_pixel_offset(n_layers, cam->width, cam->height, l);
+        for (int32_t y = 0; y < Hl; ++y)
+            for (int32_t x = 0; x < Wl; ++x) {
+                if (!mask[off + (int64_t)y * Wl + x]) continue;
+                for (int d = 1; d <= g_coarse && l + d < n_layers; ++d)
+                    m[layer_pixel_offset(n_layers, cam->width, cam->height, l + d)
+                      + (int64_t)(y >> d) * layer_w(cam->width, l + d) + (x >> d)] = 1;
+            }
+    }
+    return m;
 }
 
 /* ---------------------------------------------------------------- forward */
@@ -365,7 +441,10 @@ int oracle_forward(const oracle_camera* cam, int n_layers, int F, int64_t n, con
     memset(&S, 0, sizeof(S));
     S.cam = cam; S.n_layers = n_layers; S.F = F; S.n = n;
     S.pos = pos; S.sw = sw; S.alpha = alpha; S.desc = desc;
-    if (build_lists(&S, mask)) { free_scene(&S); return -2; }
+    uint8_t* cmask = coarse_mask(cam, n_layers, mask);
+    const int brc = build_lists(&S, cmask ? cmask : mask);
+    free(cmask);
+    if (brc) { free_scene(&S); return -2; }
 
     oracle_stats st;
     memset(&st, 0, sizeof(st));
@@ -379,18 +458,19 @@ int oracle_forward(const oracle_camera* cam, int n_layers, int F, int64_t n, con
         int64_t plane = (int64_t)Wl * Hl;
         for (int64_t q = 0; q < plane; ++q) {
             int64_t p = poff + q;
-            int64_t b = S.seg[p], e = S.seg[p + 1];
-            int64_t len = e - b;
-            int64_t K = len < ORACLE_CAP ? len : ORACLE_CAP; /* Sec. 3.2 */
+            const int in = !(mask && !mask[p]);             /* unmarked: empty (even if an ancestor) */
+            const int64_t len = in ? S.seg[p + 1] - S.seg[p] : 0;
             if (counts) counts[p] = (uint32_t)len;
             if (len > ORACLE_CAP) st.n_trunc_pixels++;
             if (len > st.max_list) st.max_list = len;
-            st.n_kept += K;
-            K = tmin_cut(&S, b, K);
+            st.n_kept += len < ORACLE_CAP ? len : ORACLE_CAP; /* Sec. 3.2 */
+            const frag_t* lst[ORACLE_CAP];
+            int64_t K = in ? blend_list(&S, l, (int32_t)(q % Wl), (int32_t)(q / Wl), p, lst) : 0;
+            K = tmin_cut(&S, lst, K);
             double T = 1.0, A = 0.0, C[64], M[64];
             for (int c = 0; c < F; ++c) { C[c] = 0.0; M[c] = 0.0; }
             for (int64_t m = 0; m < K; ++m) {                /* Eqs. (5)-(6), alpha_m = gamma (Q10) */
-                const frag_t* f = &S.frags[b + m];
+                const frag_t* f = lst[m];
                 fw_t w = frag_weights(&S, f);
                 const float* tau = desc + (int64_t)f->i * F;
                 for (int c = 0; c < F; ++c) {
@@ -408,7 +488,11 @@ int oracle_forward(const oracle_camera* cam, int n_layers, int F, int64_t n, con
             if (pyramid_mag) pyramid_mag[foff + F * plane + q] = A;
             if (kept) {
                 for (int m = 0; m < ORACLE_CAP; ++m)
-                    kept[p * ORACLE_CAP + m] = m < K ? (int32_t)S.frags[b + m].i : -1;
+                    kept[p * ORACLE_CAP + m] = m < K ? (int32_t)lst[m]->i : -1;
+            }
+            if (g_kept_layer) {
+                for (int m = 0; m < ORACLE_CAP; ++m)
+                    g_kept_layer[p * ORACLE_CAP + m] = (int8_t)(m < K ? (int)lst[m]->l - l : -1);
             }
         }
     }
@@ -439,7 +523,10 @@ int oracle_backward(const oracle_camera* cam, int n_layers, int F, int64_t n, co
     memset(&S, 0, sizeof(S));
     S.cam = cam; S.n_layers = n_layers; S.F = F; S.n = n;
     S.pos = pos; S.sw = sw; S.alpha = alpha; S.desc = desc;
-    if (build_lists(&S, mask)) { free_scene(&S); return -2; }
+    uint8_t* cmask = coarse_mask(cam, n_layers, mask);
+    const int brc = build_lists(&S, cmask ? cmask : mask);
+    free(cmask);
+    if (brc) { free_scene(&S); return -2; }
 
     /* screen-space gradients per point: (x, y, s, alpha, tau[F]) and magnitudes */
     int G = 4 + F;
@@ -452,12 +539,12 @@ int oracle_backward(const oracle_camera* cam, int n_layers, int F, int64_t n, co
         int64_t poff = layer_pixel_offset(n_layers, cam->width, cam->height, l);
         int64_t foff = poff * (F + 1);
         int64_t plane = (int64_t)Wl * Hl;
-        double lscale = ldexp(1.0, -l);                     /* d x_l / d x = 2^-l */
         for (int64_t q = 0; q < plane; ++q) {
             int64_t p = poff + q;
-            int64_t b = S.seg[p], e = S.seg[p + 1];
-            int64_t K = (e - b) < ORACLE_CAP ? (e - b) : ORACLE_CAP;
-            K = tmin_cut(&S, b, K);
+            if (mask && !mask[p]) continue;
+            const frag_t* lst[ORACLE_CAP];
+            int64_t K = blend_list(&S, l, (int32_t)(q % Wl), (int32_t)(q / Wl), p, lst);
+            K = tmin_cut(&S, lst, K);
             if (K == 0) continue;
             double gC[64], gA = (double)grad_pyramid[foff + F * plane + q];
             for (int c = 0; c < F; ++c) gC[c] = (double)grad_pyramid[foff + c * plane + q];
@@ -465,7 +552,7 @@ int oracle_backward(const oracle_camera* cam, int n_layers, int F, int64_t n, co
             double T[ORACLE_CAP + 1];
             T[0] = 1.0;
             for (int64_t m = 0; m < K; ++m) {
-                w[m] = frag_weights(&S, &S.frags[b + m]);
+                w[m] = frag_weights(&S, lst[m]);
                 T[m + 1] = T[m] * (1.0 - w[m].gamma);       /* Eq. (6) */
             }
             /* suffix recurrences: B = blend of the fragments behind m (tau and |tau|),
@@ -473,7 +560,8 @@ int oracle_backward(const oracle_camera* cam, int n_layers, int F, int64_t n, co
             double B[64], MB[64], bb = 0.0;
             for (int c = 0; c < F; ++c) { B[c] = 0.0; MB[c] = 0.0; }
             for (int64_t m = K - 1; m >= 0; --m) {
-                const frag_t* f = &S.frags[b + m];
+                const frag_t* f = lst[m];
+                const double lscale = ldexp(1.0, -(int)f->l);  /* d x_l / d x = 2^-l, l of the fragment */
                 const float* tau = desc + (int64_t)f->i * F;
                 double g = w[m].gamma, Tm = T[m];
                 /* d out / d gamma_m = T_m (<gC, tau_m - B_m> + gA (1 - bb_m)) */

@@ -356,8 +356,8 @@ def test_2k_metamorphic_relation():
 
 # ------------------------------------------------------------------ backward (P8)
 
-def _loss_f64(sc, G, pos, sw, alpha, desc):
-    r = oracle.forward(sc.cams[0], sc.n_layers, pos, sw, alpha, desc, real="double")
+def _loss_f64(sc, G, pos, sw, alpha, desc, **kw):
+    r = oracle.forward(sc.cams[0], sc.n_layers, pos, sw, alpha, desc, real="double", **kw)
     return float(np.dot(r["pyramid"], G.astype(np.float64))), r
 
 
@@ -379,13 +379,14 @@ def test_backward_zero_and_single_point():
     assert abs(g[0, 5] - gamma) < 1e-7 and g[0, 6] == 0.0
 
 
-def _fd_check(sc, seed, n_coords=60, h_rel=2.0 ** -12, tol=2e-5):
+def _fd_check(sc, seed, n_coords=60, h_rel=2.0 ** -12, tol=2e-5, **kw):
+    """kw (e.g. coarse=1) selects a variant in both the forward and the backward."""
     cam = sc.cams[0]
     P = oracle.num_pixels(cam.width, cam.height, sc.n_layers)
     G = scenes.grad_pyramid(P * (sc.F + 1), seed=seed)
-    g, mag = oracle.backward(cam, sc.n_layers, sc.pos, sc.sw, sc.alpha, sc.desc, G, real="double")
+    g, mag = oracle.backward(cam, sc.n_layers, sc.pos, sc.sw, sc.alpha, sc.desc, G, real="double", **kw)
     params = [sc.pos.copy(), sc.sw.copy(), sc.alpha.copy(), sc.desc.copy()]
-    _, base = _loss_f64(sc, G, *params)
+    _, base = _loss_f64(sc, G, *params, **kw)
     _, lev0, _ = oracle.project(cam, sc.n_layers, sc.pos, sc.sw, real="double")
     rng = np.random.default_rng(seed)
     checked = 0
@@ -410,10 +411,11 @@ def _fd_check(sc, seed, n_coords=60, h_rel=2.0 ** -12, tol=2e-5):
         for sgn in (+1, -1):
             p = [q.copy() for q in params]
             p[arr][idx] = np.float32(x0 + sgn * h)
-            L, r = _loss_f64(sc, G, *p)
+            L, r = _loss_f64(sc, G, *p, **kw)
             _, lev, _ = oracle.project(cam, sc.n_layers, p[0], p[1], real="double")
             if (not np.array_equal(r["counts"], base["counts"]) or not np.array_equal(r["kept"], base["kept"])
-                    or not np.array_equal(lev, lev0)):
+                    or not np.array_equal(lev, lev0)
+                    or ("kept_layer" in r and not np.array_equal(r["kept_layer"], base["kept_layer"]))):
                 ok = False                            # structural guard: lists/levels changed
                 break
             vals.append((L, float(p[arr][idx])))
