@@ -63,6 +63,16 @@ typedef struct {
                                   termination -- a pixel's kept list ends with the fragment
                                   after which the fp32 transmittance T = prod (1 - gamma) drops
                                   below t_min (reading Q17) */
+    int32_t coarse_layers;     /* 0 = the exact definition.  c > 0: coarse-layer inclusion
+                                  ("we include points from coarser layers
+                                  during blending (in the usual way)", reading Q22): the list
+                                  blended at pyramid pixel (l, x, y) is the 16 front-most of
+                                  the union of the fragment lists of (l + d, x >> d, y >> d),
+                                  d = 0 .. min(c, n - 1 - l), ordered by (z, i, d); each
+                                  fragment keeps its own gamma (Eq. 3 in its own layer).
+                                  Per-pixel counts and stats stay the pixel's own list.  Costs
+                                  an extra 16 keys per pyramid pixel of workspace (dense kept
+                                  lists).  c > n - 1 behaves as n - 1; c < 0 is an error. */
 } trips_config;
 
 typedef struct trips_plan trips_plan;   /* opaque, host memory, owned by the library */
@@ -92,7 +102,9 @@ typedef enum {
 /* What trips_debug_export copies (into a caller DEVICE buffer). */
 typedef enum {
     TRIPS_EXPORT_COUNTS = 1,   /* uint32[P]: per-pixel list length, pyramid pixel order     */
-    TRIPS_EXPORT_KEPT = 2      /* int32[P*16]: kept point indices in blend order, -1 padded */
+    TRIPS_EXPORT_KEPT = 2,     /* int32[P*16]: kept point indices in blend order, -1 padded */
+    TRIPS_EXPORT_KEPT_LAYER = 3 /* int32[P*16]: layer offset d of each kept entry (0 unless
+                                  coarse_layers > 0), -1 padded */
 } trips_export;
 
 /* ---- plan ------------------------------------------------------------------------- */

@@ -21,6 +21,7 @@ TRIPS_ERR_CUDA = -5
 TRIPS_FWD_SAVE_FOR_BACKWARD = 1
 TRIPS_EXPORT_COUNTS = 1
 TRIPS_EXPORT_KEPT = 2
+TRIPS_EXPORT_KEPT_LAYER = 3
 N_STAGES = 5
 STAGE_NAMES = ("count", "emit", "sort", "raster", "backward")
 
@@ -32,7 +33,8 @@ class trips_camera(C.Structure):
 
 
 class trips_config(C.Structure):
-    _fields_ = [("num_layers", C.c_int32), ("num_features", C.c_int32), ("t_min", C.c_float)]
+    _fields_ = [("num_layers", C.c_int32), ("num_features", C.c_int32), ("t_min", C.c_float),
+                ("coarse_layers", C.c_int32)]
 
 
 class trips_stats(C.Structure):
@@ -105,8 +107,8 @@ def check(status, where):
 
 # ---- same names as include/trips.h -------------------------------------------------
 
-def trips_plan_create(num_layers, num_features, width, height, max_points, t_min=0.0):
-    cfg = trips_config(num_layers, num_features, t_min)
+def trips_plan_create(num_layers, num_features, width, height, max_points, t_min=0.0, coarse_layers=0):
+    cfg = trips_config(num_layers, num_features, t_min, coarse_layers)
     out = _VP()
     check(lib().trips_plan_create(C.byref(cfg), width, height, max_points, C.byref(out)), "trips_plan_create")
     return out.value

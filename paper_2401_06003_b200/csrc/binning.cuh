@@ -168,7 +168,8 @@ __global__ void __launch_bounds__(1024) k_tscan(Params P)
     for (int base = 0; base < T; base += blockDim.x) {
         const int t = base + threadIdx.x;
         const uint32_t a = t < T ? P.tile_off[t] : 0u;
-        const uint32_t b = min(4u * a, (uint32_t)(kTilePix * kCap));
+        // coarse inclusion: dense 16 per pixel (a pixel's merged list can exceed its own)
+        const uint32_t b = P.coarse ? (uint32_t)(kTilePix * kCap) : min(4u * a, (uint32_t)(kTilePix * kCap));
         uint32_t ta, tb;
         const uint32_t pa = block_excl_scan(a, s_ws, &ta);
         const uint32_t pb = block_excl_scan(t < T ? b : 0u, s_ws, &tb);

@@ -39,6 +39,7 @@ struct Params {
     int32_t n, F, FC, RS, G;          // F features, FC = round_up(F,4), RS = 4 + FC, G = 8 + FC
     int32_t n_layers, T;              // layers, total tiles
     float t_min;                      // T_min blend variant (0 = the exact definition)
+    int32_t coarse;                   // coarse-layer inclusion depth (0 = the exact definition)
     LayerGeom L[kMaxLayers];
     Cam cam;
     // inputs (caller)
@@ -54,7 +55,9 @@ struct Params {
     uint16_t* bin_orig;    // [8n]     footprint origin in the tile: (qx0+1) | (qy0+1) << 5
     uint32_t* pix_cnt;     // [T*256]  list length per tile pixel
     uint32_t* pix_meta;    // [T*256]  (local kept offset << 5) | K
-    uint64_t* kept;        // [kcap]   kept (z, i) keys, per pixel in blend order
+    uint64_t* kept;        // [kcap]   kept (z, i) keys, per pixel in blend order; with coarse
+                           //          inclusion (z, i << 4 | d), dense 16 per pixel
+    uint64_t* own;         // [T*256*16] coarse inclusion only: each pixel's own sorted top-16
     float* kept_gamma;     // [kcap]   gamma of each kept fragment (saved for the backward)
     unsigned long long* stats;  // [8]  n_culled, n_visible, n_pairs, n_frag, n_kept, n_trunc, max_list
 };

@@ -159,9 +159,16 @@ __device__ __forceinline__ TileCoord tile_coord(const Params& P, int t)
 // 64 KB per CTA shrinks L1 -- profiles/r01_v2.md.)
 __host__ __device__ constexpr int raster_dyn_smem() { return kChunk * 32; }
 
-template <int FC>
+// MODE: kRasterPlain (the definition), kRasterTmin (T_min variant, Q17) or kRasterOwn
+// (coarse-layer inclusion, Q22: phases A-C only; the pixel's own sorted top-16 goes to P.own
+// and k_coarse_blend merges it with its ancestors' lists and blends).
+enum RasterMode { kRasterPlain = 0, kRasterTmin = 1, kRasterOwn = 2 };
+
+template <int FC, int MODE>
 __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P, float* __restrict__ pyramid, int save)
 {
+    constexpr bool COARSE = MODE == kRasterOwn;
+    constexpr bool TMIN = MODE == kRasterTmin;
     extern __shared__ __align__(16) uint64_t s_dyn[];
     uint64_t* s_keys = s_dyn;                        // [kChunk * 4] fragment keys of a chunk
     __shared__ uint32_t s_cnt[kTilePix];
@@ -314,6 +321,16 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
         TRIPS_PCLK(3);
     }
 
+    if constexpr (COARSE) {
+        P.pix_cnt[(size_t)t * kTilePix + tid] = valid ? total : 0u;
+        const int Ko = valid ? (int)min(total, (uint32_t)kCap) : 0;
+        uint64_t* op = P.own + ((size_t)t * kTilePix + tid) * kCap;
+#pragma unroll
+        for (int mm = 0; mm < kCap; ++mm)
+            if (mm < Ko) op[mm] = r[mm];
+        return;
+    }
+
     // phase D: front-to-back blend of the kept list (Eqs. 5-6; alpha_m := gamma_m, Q10).
     // Record gathers are issued kBatch at a time.  Without a following backward the loop
     // stops once T == 0 exactly (later terms vanish); with one, every gamma_m is needed.
@@ -359,7 +376,7 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
                 A += tg;
                 T = __fmul_rn(T, __fsub_rn(1.0f, w.gamma));      // pinned: decides the T_min cut
                 if (save) P.kept_gamma[kidx + mm] = w.gamma;
-                if (T < P.t_min) Keff = mm + 1;
+                if (TMIN && T < P.t_min) Keff = mm + 1;
             }
         }
     }
@@ -385,11 +402,113 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
     TRIPS_PCLK(6);
 }
 
+// --------------------------------------------------------------------------- K4c coarse blend
+
+// Coarse-layer inclusion (reading Q22).  One thread
+// per pyramid pixel (l, x, y): merges the own sorted top-16 lists of (l + d, x >> d, y >> d),
+// d = 0..D, into the top-16 of their union.  Keys become (z, i << 4 | d) so that the networks
+// order by (z, i, d) -- the same point's fragment in a finer layer first (i < 2^28 by the plan
+// limit).  The top-16 of a union is inside the union of the top-16s, so the own lists suffice.
+// Then the front-to-back blend of k_raster phase D, each fragment weighted in its own layer and
+// pixel; kept lists are dense (16 per pixel, tile_kbase[t] = 4096 t).
+template <int FC>
+__global__ void __launch_bounds__(kTilePix) k_coarse_blend(Params P, float* __restrict__ pyramid, int save)
+{
+    const int t = blockIdx.x;
+    const TileCoord tc = tile_coord(P, t);
+    const LayerGeom& G = P.L[tc.l];
+    const int tid = threadIdx.x;
+    const int px = tc.tx * kTile + (tid & (kTile - 1)), py = tc.ty * kTile + (tid >> 4);
+    const bool valid = px < G.W && py < G.H;
+    const int D = min(P.coarse, P.n_layers - 1 - tc.l);
+
+    uint64_t r[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) r[j] = kKeyMax;
+    int K = 0;
+    for (int d = 0; d <= D; ++d) {
+        const LayerGeom& A = P.L[tc.l + d];
+        const int ax = px >> d, ay = py >> d;
+        const size_t slot = (size_t)(A.tile_base + (ay >> 4) * A.tiles_x + (ax >> 4)) * kTilePix
+                          + (size_t)((ay & (kTile - 1)) * kTile + (ax & (kTile - 1)));
+        const int kd = valid ? (int)min(__ldg(P.pix_cnt + slot), (uint32_t)kCap) : 0;
+        if (__all_sync(0xffffffffu, kd == 0)) continue;
+        K += kd;
+        const uint64_t* op = P.own + slot * kCap;
+        uint64_t tk[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const uint64_t k = j < kd ? __ldg(reinterpret_cast<const unsigned long long*>(op) + j) : kKeyMax;
+            tk[j] = j < kd ? ((k & 0xffffffff00000000ull) | ((k & 0xffffffffull) << 4) | (uint64_t)d) : kKeyMax;
+        }
+        merge_keep16<16>(r, tk);
+    }
+    K = min(K, kCap);
+
+    const size_t kidx = (size_t)P.tile_kbase[t] + (size_t)tid * kCap;
+    constexpr int kR4 = 1 + FC / 4;
+    float C[FC];
+#pragma unroll
+    for (int c = 0; c < FC; ++c) C[c] = 0.f;
+    float A = 0.f, T = 1.f;
+    int Keff = K;
+#pragma unroll
+    for (int b = 0; b < kCap / kBlendBatch; ++b) {
+        if (b * kBlendBatch >= Keff || (!save && T == 0.f)) break;
+        float4 rb[kBlendBatch][1 + FC / 4];
+#pragma unroll
+        for (int u = 0; u < kBlendBatch; ++u) {
+            const int mm = b * kBlendBatch + u;
+            const uint32_t ii = (uint32_t)(mm < K ? r[mm] : r[0]) >> 4;
+            const float4* rp = reinterpret_cast<const float4*>(P.rec + (size_t)ii * P.RS);
+#pragma unroll
+            for (int c4 = 0; c4 < kR4; ++c4) rb[u][c4] = __ldg(rp + c4);
+        }
+#pragma unroll
+        for (int u = 0; u < kBlendBatch; ++u) {
+            const int mm = b * kBlendBatch + u;
+            if (mm < Keff) {
+                const int d = (int)(r[mm] & 15u);
+                const FragW w = frag_weights(rb[u][0], tc.l + d, P.n_layers, px >> d, py >> d);
+                const float tg = T * w.gamma;
+#pragma unroll
+                for (int c4 = 0; c4 < FC / 4; ++c4) {
+                    const float4 tau = rb[u][1 + c4];
+                    C[4 * c4 + 0] = fmaf(tg, tau.x, C[4 * c4 + 0]);
+                    C[4 * c4 + 1] = fmaf(tg, tau.y, C[4 * c4 + 1]);
+                    C[4 * c4 + 2] = fmaf(tg, tau.z, C[4 * c4 + 2]);
+                    C[4 * c4 + 3] = fmaf(tg, tau.w, C[4 * c4 + 3]);
+                }
+                A += tg;
+                T = __fmul_rn(T, __fsub_rn(1.0f, w.gamma));
+                if (save) P.kept_gamma[kidx + mm] = w.gamma;
+                if (T < P.t_min) Keff = mm + 1;
+            }
+        }
+    }
+    if (valid) {
+        const int64_t plane = (int64_t)G.W * G.H;
+        float* out = pyramid + G.float_off + (int64_t)py * G.W + px;
+#pragma unroll
+        for (int c = 0; c < FC; ++c)
+            if (c < P.F) out[c * plane] = C[c];
+        out[P.F * plane] = A;
+    }
+    P.pix_meta[(size_t)t * kTilePix + tid] = ((uint32_t)(tid * kCap) << 5) | (uint32_t)Keff;
+    if (save) {
+        uint64_t* kp = P.kept + kidx;
+#pragma unroll
+        for (int mm = 0; mm < kCap; ++mm)
+            if (mm < Keff) kp[mm] = r[mm];
+    }
+}
+
 // --------------------------------------------------------------------------- K5 backward
 
 // CAM: also accumulate the camera gradient:
 // grad_cam[17] += (dR row-major, dt, dfx, dfy, dcx, dcy, df), one block reduction per tile.
-template <int FC, bool CAM>
+// COARSE: kept keys are (z, i << 4 | d) and fragment m lives in layer l + d at (x >> d, y >> d).
+template <int FC, bool CAM, bool COARSE>
 __global__ void __launch_bounds__(kTilePix) k_backward(Params P, const float* __restrict__ gpyr,
                                                        float* __restrict__ grad, float* __restrict__ grad_cam)
 {
@@ -432,7 +551,7 @@ __global__ void __launch_bounds__(kTilePix) k_backward(Params P, const float* __
 #pragma unroll
     for (int c = 0; c < FC; ++c) B[c] = 0.f;
     float bb = 0.f;
-    const float sc = pow2_neg(tc.l);
+    const float sc0 = pow2_neg(tc.l);
     const Cam& cam = P.cam;
 #pragma unroll
     for (int b = kCap / kBatch - 1; b >= 0; --b) {
@@ -443,7 +562,8 @@ __global__ void __launch_bounds__(kTilePix) k_backward(Params P, const float* __
         for (int u = 0; u < kBatch; ++u) {
             const int mm = min(b * kBatch + u, K - 1);
             kb[u] = __ldg(reinterpret_cast<const unsigned long long*>(kp) + mm);
-            const float4* rp = reinterpret_cast<const float4*>(P.rec + (size_t)(uint32_t)kb[u] * P.RS);
+            const uint32_t iu = COARSE ? (uint32_t)kb[u] >> 4 : (uint32_t)kb[u];
+            const float4* rp = reinterpret_cast<const float4*>(P.rec + (size_t)iu * P.RS);
 #pragma unroll
             for (int c4 = 0; c4 <= FC / 4; ++c4) rb[u][c4] = __ldg(rp + c4);
         }
@@ -451,10 +571,12 @@ __global__ void __launch_bounds__(kTilePix) k_backward(Params P, const float* __
         for (int u = kBatch - 1; u >= 0; --u) {
             const int mm = b * kBatch + u;
             if (mm >= K) continue;
-            const uint32_t i = (uint32_t)kb[u];
+            const uint32_t i = COARSE ? (uint32_t)kb[u] >> 4 : (uint32_t)kb[u];
+            const int d = COARSE ? (int)(kb[u] & 15u) : 0;
+            const float sc = COARSE ? pow2_neg(tc.l + d) : sc0;
             const float z = __uint_as_float((uint32_t)(kb[u] >> 32));
             const float4 r0 = rb[u][0];
-            const FragW w = frag_weights(r0, tc.l, P.n_layers, px, py);
+            const FragW w = frag_weights(r0, tc.l + d, P.n_layers, px >> d, py >> d);
             const float g = gam[mm], tm = Tm[mm];
             float tau[FC];
 #pragma unroll
@@ -554,7 +676,11 @@ __global__ void __launch_bounds__(kTilePix) k_export(Params P, int what, void* d
         const int K = (int)(meta & 31u);
         const uint64_t* kp = P.kept + P.tile_kbase[t] + (meta >> 5);
         int32_t* o = static_cast<int32_t*>(dst) + pidx * kCap;
-        for (int m = 0; m < kCap; ++m) o[m] = m < K ? (int32_t)(uint32_t)kp[m] : -1;
+        for (int m = 0; m < kCap; ++m) {
+            const uint32_t lo = (uint32_t)kp[m];
+            if (what == 3) o[m] = m < K ? (P.coarse ? (int32_t)(lo & 15u) : 0) : -1;
+            else o[m] = m < K ? (int32_t)(P.coarse ? lo >> 4 : lo) : -1;
+        }
     }
 }
 

@@ -34,13 +34,14 @@ struct EventPair {
 struct trips_plan {
     int32_t n_layers, F, FC, RS, G, W, H, T;
     float t_min;
+    int32_t coarse;         // coarse-layer inclusion depth, clamped to n_layers - 1
     int64_t max_points, P, pyr_floats;
     LayerGeom L[kMaxLayers];
     uint64_t kcap;
     // workspace layout (byte offsets)
     int32_t ctas;           // binning CTAs (persistent grid)
     size_t off_rec, off_z, off_hist, off_cvis, off_toff, off_tkb, off_bkey, off_borig, off_pcnt, off_pmeta, off_kept, off_kgam,
-        off_stats, ws_bytes;
+        off_own, off_stats, ws_bytes;
     // state
     const void* ws_bound = nullptr;
     int stage = 0;          // 0 none, 1 projected, 2 forward (saved), 3 forward (not saved)
@@ -145,6 +146,7 @@ Params make_params(const trips_plan* p, void* ws)
     P.F = p->F; P.FC = p->FC; P.RS = p->RS; P.G = p->G;
     P.n_layers = p->n_layers; P.T = p->T;
     P.t_min = p->t_min;
+    P.coarse = p->coarse;
     for (int l = 0; l < kMaxLayers; ++l) P.L[l] = p->L[l];
     P.cam = p->cam;
     char* b = static_cast<char*>(ws);
@@ -160,6 +162,7 @@ Params make_params(const trips_plan* p, void* ws)
     P.pix_meta = reinterpret_cast<uint32_t*>(b + p->off_pmeta);
     P.kept = reinterpret_cast<uint64_t*>(b + p->off_kept);
     P.kept_gamma = reinterpret_cast<float*>(b + p->off_kgam);
+    P.own = p->coarse ? reinterpret_cast<uint64_t*>(b + p->off_own) : nullptr;
     P.stats = reinterpret_cast<unsigned long long*>(b + p->off_stats);
     return P;
 }
@@ -191,11 +194,13 @@ int trips_plan_create(const trips_config* cfg, int32_t width, int32_t height, in
     const int n = cfg->num_layers, F = cfg->num_features;
     if (n < 1 || n > kMaxLayers || F < 1 || F > 32) return TRIPS_ERR_ARG;
     if (!(cfg->t_min >= 0.0f && cfg->t_min < 1.0f)) return TRIPS_ERR_ARG;
+    if (cfg->coarse_layers < 0) return TRIPS_ERR_ARG;
     if (width < 1 || height < 1 || width > 32768 || height > 32768) return TRIPS_ERR_ARG;
     if (max_points < 0 || max_points >= (int64_t(1) << 28)) return TRIPS_ERR_ARG;
     trips_plan* p = new trips_plan();
     p->n_layers = n; p->F = F; p->FC = (F + 3) & ~3; p->RS = 4 + p->FC; p->G = 8 + p->FC;
     p->t_min = cfg->t_min;
+    p->coarse = std::min(cfg->coarse_layers, n - 1);
     p->W = width; p->H = height; p->max_points = max_points;
     memset(p->L, 0, sizeof(p->L));
     int64_t pix = 0;
@@ -216,7 +221,7 @@ int trips_plan_create(const trips_config* cfg, int32_t width, int32_t height, in
     p->T = tiles;
     p->pyr_floats = pix * (F + 1);
     const uint64_t kc1 = (uint64_t)tiles * kTilePix * kCap, kc2 = (uint64_t)max_points * 32;
-    p->kcap = kc1 < kc2 ? kc1 : kc2;
+    p->kcap = (p->coarse || kc1 < kc2) ? kc1 : kc2;    // coarse inclusion: dense 16 per pixel
     if (p->kcap >= (uint64_t(1) << 32) || tiles > kMaxTilesSmem) { delete p; return TRIPS_ERR_ARG; }
     const size_t N = (size_t)(max_points > 0 ? max_points : 1);
     size_t o = 0;
@@ -233,6 +238,7 @@ int trips_plan_create(const trips_config* cfg, int32_t width, int32_t height, in
     p->off_pmeta = o; o = align256(o + (size_t)tiles * kTilePix * 4);
     p->off_kept = o;  o = align256(o + (p->kcap ? p->kcap : 1) * 8);
     p->off_kgam = o;  o = align256(o + (p->kcap ? p->kcap : 1) * 4);
+    p->off_own = o;   o = align256(o + (p->coarse ? (size_t)tiles * kTilePix * kCap * 8 : 0));
     p->off_stats = o; o = align256(o + S_COUNT * 8);
     p->ws_bytes = o;
     *out = p;
@@ -321,13 +327,28 @@ int trips_splat_forward(trips_plan* p, void* ws, float* pyramid, uint32_t flags,
         StageScope sc(p, 3, st);
         const int save = (flags & TRIPS_FWD_SAVE_FOR_BACKWARD) ? 1 : 0;
         const size_t rsm = (size_t)raster_dyn_smem();
-        static bool rattr[9] = {};
-        if (!rattr[p->FC / 4]) {
-            TRIPS_FC_SWITCH(p->FC, (cudaFuncSetAttribute(k_raster<kFC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                         (int)rsm)));
-            rattr[p->FC / 4] = true;
+        static bool rattr[3][9] = {};
+        const int mode = p->coarse ? kRasterOwn : (p->t_min > 0.f ? kRasterTmin : kRasterPlain);
+        if (!rattr[mode][p->FC / 4]) {
+            const int a = (int)cudaFuncAttributeMaxDynamicSharedMemorySize;
+            if (mode == kRasterOwn) {
+                TRIPS_FC_SWITCH(p->FC, (cudaFuncSetAttribute(k_raster<kFC, kRasterOwn>, (cudaFuncAttribute)a, (int)rsm)));
+            } else if (mode == kRasterTmin) {
+                TRIPS_FC_SWITCH(p->FC, (cudaFuncSetAttribute(k_raster<kFC, kRasterTmin>, (cudaFuncAttribute)a, (int)rsm)));
+            } else {
+                TRIPS_FC_SWITCH(p->FC, (cudaFuncSetAttribute(k_raster<kFC, kRasterPlain>, (cudaFuncAttribute)a, (int)rsm)));
+            }
+            rattr[mode][p->FC / 4] = true;
         }
-        TRIPS_FC_SWITCH(p->FC, (k_raster<kFC><<<p->T, kTilePix, rsm, st>>>(P, pyramid, save)));
+        if (mode == kRasterOwn) {
+            TRIPS_FC_SWITCH(p->FC, (k_raster<kFC, kRasterOwn><<<p->T, kTilePix, rsm, st>>>(P, pyramid, save)));
+            if ((rc = check_launch())) return rc;
+            TRIPS_FC_SWITCH(p->FC, (k_coarse_blend<kFC><<<p->T, kTilePix, 0, st>>>(P, pyramid, save)));
+        } else if (mode == kRasterTmin) {
+            TRIPS_FC_SWITCH(p->FC, (k_raster<kFC, kRasterTmin><<<p->T, kTilePix, rsm, st>>>(P, pyramid, save)));
+        } else {
+            TRIPS_FC_SWITCH(p->FC, (k_raster<kFC, kRasterPlain><<<p->T, kTilePix, rsm, st>>>(P, pyramid, save)));
+        }
         if ((rc = check_launch())) return rc;
     }
     p->stage = (flags & TRIPS_FWD_SAVE_FOR_BACKWARD) ? 2 : 3;
@@ -345,12 +366,18 @@ int trips_splat_backward(trips_plan* p, void* ws, const float* grad_pyramid, flo
     int rc;
     {
         StageScope sc(p, 4, st);
-        if (grad_camera) {
-            TRIPS_FC_SWITCH(p->FC, (k_backward<kFC, true><<<p->T, kTilePix, 0, st>>>(P, grad_pyramid, grad,
-                                                                                       grad_camera)));
+        if (grad_camera && p->coarse) {
+            TRIPS_FC_SWITCH(p->FC, (k_backward<kFC, true, true><<<p->T, kTilePix, 0, st>>>(P, grad_pyramid, grad,
+                                                                                             grad_camera)));
+        } else if (grad_camera) {
+            TRIPS_FC_SWITCH(p->FC, (k_backward<kFC, true, false><<<p->T, kTilePix, 0, st>>>(P, grad_pyramid, grad,
+                                                                                              grad_camera)));
+        } else if (p->coarse) {
+            TRIPS_FC_SWITCH(p->FC, (k_backward<kFC, false, true><<<p->T, kTilePix, 0, st>>>(P, grad_pyramid, grad,
+                                                                                              nullptr)));
         } else {
-            TRIPS_FC_SWITCH(p->FC, (k_backward<kFC, false><<<p->T, kTilePix, 0, st>>>(P, grad_pyramid, grad,
-                                                                                        nullptr)));
+            TRIPS_FC_SWITCH(p->FC, (k_backward<kFC, false, false><<<p->T, kTilePix, 0, st>>>(P, grad_pyramid, grad,
+                                                                                               nullptr)));
         }
         if ((rc = check_launch())) return rc;
     }
@@ -388,9 +415,10 @@ int trips_read_stats(const trips_plan* p, const void* ws, trips_stats* out, void
 int trips_debug_export(const trips_plan* p, const void* ws, int32_t what, void* dst, void* stream)
 {
     if (!p || !ws || !dst) return TRIPS_ERR_ARG;
-    if (what != TRIPS_EXPORT_COUNTS && what != TRIPS_EXPORT_KEPT) return TRIPS_ERR_ARG;
+    if (what != TRIPS_EXPORT_COUNTS && what != TRIPS_EXPORT_KEPT && what != TRIPS_EXPORT_KEPT_LAYER)
+        return TRIPS_ERR_ARG;
     if (ws != p->ws_bound || p->stage < 2) return TRIPS_ERR_STATE;
-    if (what == TRIPS_EXPORT_KEPT && p->stage != 2) return TRIPS_ERR_STATE;
+    if (what != TRIPS_EXPORT_COUNTS && p->stage != 2) return TRIPS_ERR_STATE;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     Params P = make_params(p, const_cast<void*>(ws));
     k_export<<<p->T, kTilePix, 0, st>>>(P, what, dst);

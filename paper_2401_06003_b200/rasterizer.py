@@ -31,15 +31,17 @@ def _check_input(name, t, shape_tail=()):
 class Rasterizer:
     """One plan + one workspace (one in-flight view).  Not thread-safe."""
 
-    def __init__(self, width, height, num_layers=4, num_features=4, max_points=1 << 20, device=None, t_min=0.0):
+    def __init__(self, width, height, num_layers=4, num_features=4, max_points=1 << 20, device=None, t_min=0.0,
+                 coarse_layers=0):
         self.width, self.height = int(width), int(height)
         self.num_layers, self.F = int(num_layers), int(num_features)
         self.max_points = int(max_points)
         self.device = torch.device(device if device is not None else "cuda")
         A.lib()
         self.t_min = float(t_min)
+        self.coarse_layers = int(coarse_layers)
         self.plan = A.trips_plan_create(self.num_layers, self.F, self.width, self.height, self.max_points,
-                                        self.t_min)
+                                        self.t_min, self.coarse_layers)
         self.ws = torch.empty(A.trips_workspace_bytes(self.plan), dtype=torch.uint8, device=self.device)
         self.P = A.trips_num_pixels(self.plan)
         self.pyramid_floats = A.trips_pyramid_floats(self.plan)
@@ -114,6 +116,13 @@ class Rasterizer:
     def export_kept(self):
         dst = torch.empty(self.P * 16, dtype=torch.int32, device=self.device)
         A.check(A.trips_debug_export(self.plan, self.ws.data_ptr(), A.TRIPS_EXPORT_KEPT, dst.data_ptr(),
+                                     _stream_handle()), "trips_debug_export")
+        return dst.view(self.P, 16)
+
+    def export_kept_layer(self):
+        """Layer offset d of each kept entry (coarse-layer inclusion), -1 padded."""
+        dst = torch.empty(self.P * 16, dtype=torch.int32, device=self.device)
+        A.check(A.trips_debug_export(self.plan, self.ws.data_ptr(), A.TRIPS_EXPORT_KEPT_LAYER, dst.data_ptr(),
                                      _stream_handle()), "trips_debug_export")
         return dst.view(self.P, 16)
 

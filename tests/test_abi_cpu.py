@@ -58,13 +58,21 @@ def test_plan_geometry(A):
     plan = A.trips_plan_create(8, 4, 1920, 1080, 10)
     try:
         assert A.trips_num_pixels(plan) == 2_764_845           # P at 1080p, n=8
+        small = A.trips_workspace_bytes(plan)
+    finally:
+        A.trips_plan_destroy(plan)
+    # coarse-layer inclusion: + dense kept lists and own lists, 16 per tile pixel
+    plan = A.trips_plan_create(8, 4, 1920, 1080, 10, 0.0, 20)
+    try:
+        assert A.trips_workspace_bytes(plan) >= small + 2_764_845 * 16 * (8 + 8 + 4)
     finally:
         A.trips_plan_destroy(plan)
 
 
 @pytest.mark.parametrize("args", [(0, 4, 64, 64, 10), (17, 4, 64, 64, 10), (4, 0, 64, 64, 10),
                                   (4, 33, 64, 64, 10), (4, 4, 0, 64, 10), (4, 4, 64, 64, -1),
-                                  (4, 4, 64, 64, 1 << 28)])
+                                  (4, 4, 64, 64, 1 << 28), (4, 4, 64, 64, 10, -0.1), (4, 4, 64, 64, 10, 1.0),
+                                  (4, 4, 64, 64, 10, 0.0, -1)])
 def test_plan_create_rejects(A, args):
     with pytest.raises(A.TripsError) as e:
         A.trips_plan_create(*args)

@@ -31,10 +31,16 @@ def T(a, dev):
     return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
 
 
-def gpu_run(sc, dev, cam=None, G=None, save=True, export=True, t_min=0.0):
+def _ovar(var):
+    """Rasterizer variant kwargs -> oracle kwargs."""
+    return dict(t_min=var.get("t_min", 0.0), coarse=var.get("coarse_layers", 0))
+
+
+def gpu_run(sc, dev, cam=None, G=None, save=True, export=True, **var):
+    """var: Rasterizer variant options (t_min, coarse_layers)."""
     from paper_2401_06003_b200 import Rasterizer
     cam = cam or sc.cams[0]
-    r = Rasterizer(cam.width, cam.height, sc.n_layers, sc.F, max_points=max(sc.n, 1), device=dev, t_min=t_min)
+    r = Rasterizer(cam.width, cam.height, sc.n_layers, sc.F, max_points=max(sc.n, 1), device=dev, **var)
     pos, sw, al, de = (T(a, dev) for a in (sc.pos, sc.sw, sc.alpha, sc.desc))
     level = torch.empty(sc.n, dtype=torch.int8, device=dev)
     proj = torch.empty(sc.n, 4, dtype=torch.float32, device=dev)
@@ -45,6 +51,8 @@ def gpu_run(sc, dev, cam=None, G=None, save=True, export=True, t_min=0.0):
         out["counts"] = r.export_counts().cpu().numpy().astype(np.uint32)
         if save:
             out["kept"] = r.export_kept().cpu().numpy()
+            if var.get("coarse_layers", 0):
+                out["kept_layer"] = r.export_kept_layer().cpu().numpy()
     if G is not None:
         g = r.backward(T(G, dev))
         gg = g.cpu().numpy()
@@ -55,9 +63,9 @@ def gpu_run(sc, dev, cam=None, G=None, save=True, export=True, t_min=0.0):
     return out
 
 
-def check_forward(sc, got, cam=None, mask=None):
+def check_forward(sc, got, cam=None, mask=None, **var):
     cam = cam or sc.cams[0]
-    ref = oracle.forward(cam, sc.n_layers, sc.pos, sc.sw, sc.alpha, sc.desc, mask=mask)
+    ref = oracle.forward(cam, sc.n_layers, sc.pos, sc.sw, sc.alpha, sc.desc, mask=mask, **_ovar(var))
     proj, level, _ = oracle.project(cam, sc.n_layers, sc.pos, sc.sw)
     # bit-exact block
     assert np.array_equal(got["level"], level), "level codes differ"
@@ -66,6 +74,8 @@ def check_forward(sc, got, cam=None, mask=None):
         assert np.array_equal(got["counts"], ref["counts"]), "counts differ"
         if "kept" in got:
             assert np.array_equal(got["kept"], ref["kept"]), "kept lists differ"
+        if "kept_layer" in got:
+            assert np.array_equal(got["kept_layer"], ref["kept_layer"].astype(np.int32)), "kept layers differ"
         st = got["stats"]
         for k in ("n_culled", "n_visible", "n_frag", "n_kept", "n_trunc_pixels", "max_list"):
             assert st[k] == ref["stats"][k], (k, st[k], ref["stats"][k])
@@ -76,6 +86,8 @@ def check_forward(sc, got, cam=None, mask=None):
         assert np.array_equal(got["counts"][pix], ref["counts"][pix]), "counts differ (sampled)"
         if "kept" in got:
             assert np.array_equal(got["kept"][pix], ref["kept"][pix]), "kept lists differ (sampled)"
+        if "kept_layer" in got:
+            assert np.array_equal(got["kept_layer"][pix], ref["kept_layer"][pix].astype(np.int32))
         F1 = sc.F + 1
         sel = pixel_float_index(cam, sc.n_layers, F1, pix)
     err = np.abs(got["pyr"].astype(np.float64)[sel] - ref["pyramid"][sel])
@@ -97,9 +109,9 @@ def pixel_float_index(cam, n_layers, F1, pix):
     return np.concatenate(out)
 
 
-def check_backward(sc, got, G, cam=None, mask=None):
+def check_backward(sc, got, G, cam=None, mask=None, **var):
     cam = cam or sc.cams[0]
-    g, gm = oracle.backward(cam, sc.n_layers, sc.pos, sc.sw, sc.alpha, sc.desc, G, mask=mask)
+    g, gm = oracle.backward(cam, sc.n_layers, sc.pos, sc.sw, sc.alpha, sc.desc, G, mask=mask, **_ovar(var))
     err = np.abs(got["grad"] - g)
     bad = err > GRAD_TOL * gm + 1e-30
     assert not bad.any(), f"{bad.sum()} gradient entries out of tolerance; worst rel " \
@@ -147,7 +159,7 @@ def test_adversarial_scene(dev):
     assert got["stats"]["max_list"] >= 40
 
 
-@pytest.mark.parametrize("F", [1, 3, 5, 8, 13])
+@pytest.mark.parametrize("F", [1, 3, 5, 6, 8, 13])
 def test_feature_counts(dev, F):
     sc = scenes.tiny_scene(3, n=500, F=F, W=50, H=37, n_layers=4)
     G = grads_for(sc, sc.cams[0], seed=F)
@@ -418,3 +430,61 @@ def test_camera_gradient_adversarial_and_full_size(dev):
     _camera_grad_case(scenes.adversarial_scene(), dev)
     sc = scenes.make_config("C3", n=1_000_000)
     _camera_grad_case(sc, dev, mask=_sample_mask(sc.cams[0], sc.n_layers, seed=9))
+
+
+# ------------------------------------------------------------------ coarse-layer inclusion
+
+def _coarse_cases():
+    yield "c1", scenes.c1(), 3
+    yield "adv", scenes.adversarial_scene(), 1
+    yield "dense", scenes.tiny_scene(11, n=30000, F=4, W=40, H=24, n_layers=3), 2
+    yield "f6", scenes.tiny_scene(3, n=800, F=6, W=50, H=37, n_layers=5), 4
+    for seed in range(6):
+        yield f"tiny{seed}", scenes.tiny_scene(seed), 1 + seed % 3
+
+
+@pytest.mark.parametrize("case", range(10))
+def test_coarse_inclusion(dev, case):
+    """SURVEY.md 8(f) row 3 / reading Q22: bit-exact own counts, merged kept lists and their
+    layer offsets; features and gradients within the north-star tolerances."""
+    name, sc, c = list(_coarse_cases())[case]
+    G = grads_for(sc, sc.cams[0], seed=case)
+    got = gpu_run(sc, dev, G=G, coarse_layers=c)
+    check_forward(sc, got, coarse_layers=c)
+    check_backward(sc, got, G, coarse_layers=c)
+    if sc.n_layers > 1 and got["stats"]["n_frag"] > 100:
+        assert (got["kept_layer"] > 0).any(), name                  # coarse fragments were merged
+
+
+def test_coarse_with_tmin_and_camera_gradient(dev):
+    from paper_2401_06003_b200 import Rasterizer
+    sc = scenes.tiny_scene(11, n=30000, F=4, W=40, H=24, n_layers=3)
+    cam = sc.cams[0]
+    G = grads_for(sc, cam, seed=8)
+    got = gpu_run(sc, dev, G=G, coarse_layers=2, t_min=0.1)
+    check_forward(sc, got, coarse_layers=2, t_min=0.1)
+    check_backward(sc, got, G, coarse_layers=2, t_min=0.1)
+    r = Rasterizer(cam.width, cam.height, sc.n_layers, sc.F, max_points=sc.n, device=dev, coarse_layers=2)
+    pos, sw, al, de = (T(a, dev) for a in (sc.pos, sc.sw, sc.alpha, sc.desc))
+    r.project(cam, pos, sw, al, de)
+    r.forward(save=True)
+    gc = torch.zeros(17, device=dev)
+    r.backward(T(G, dev), grad_camera=gc)
+    ref, refm = np.zeros(17), np.zeros(17)
+    oracle.backward(cam, sc.n_layers, sc.pos, sc.sw, sc.alpha, sc.desc, G, grad_cam=ref, grad_cam_mag=refm,
+                    coarse=2)
+    assert np.all(np.abs(gc.cpu().numpy() - ref) <= GRAD_TOL * refm + 1e-30)
+
+
+def test_coarse_full_size_c3_sampled(dev):
+    """C3 (6M points, 8 layers, wide sizes) in the bench launch configuration with every
+    coarser layer included; oracle on sampled pixels (their ancestors' lists are built)."""
+    sc = scenes.make_config("C3")
+    cam = sc.cams[0]
+    mask = _sample_mask(cam, sc.n_layers, seed=33, n_random=1500)
+    G = grads_for(sc, cam, seed=2, mask=mask)
+    got = gpu_run(sc, dev, G=G, coarse_layers=7)
+    check_forward(sc, got, mask=mask, coarse_layers=7)
+    check_backward(sc, got, G, mask=mask, coarse_layers=7)
+    plain = gpu_run(sc, dev, export=True)
+    assert np.array_equal(plain["counts"], got["counts"])          # counts stay the own lists
