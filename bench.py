@@ -287,6 +287,43 @@ def run_cuda(args, rank, world, local_rank):
         rast.set_profiling(False)
         cam_ms["with_camera_grad" if with_cam else "without"] = st_["backward"][0] / max(st_["backward"][1], 1)
 
+    # ---- side measurement: blend variants and feature counts, per view
+    def per_view_ms(r, desc, views):
+        gp = torch.from_numpy(scenes.grad_pyramid(r.pyramid_floats, seed=100)).to(dev)
+        gb = torch.zeros(n, r.G, dtype=torch.float32, device=dev)
+        for v in views[:2]:                                          # warm-up
+            r.project(sc.cams[v], d["pos"], d["sw"], d["alpha"], desc)
+            r.forward(save=True)
+            r.backward(gp, gb)
+        torch.cuda.synchronize()
+        r.stage_ms(reset=True)
+        r.set_profiling(True)
+        for v in views:
+            r.project(sc.cams[v], d["pos"], d["sw"], d["alpha"], desc)
+            r.forward(save=True)
+            r.backward(gp, gb)
+        torch.cuda.synchronize()
+        st_ = r.stage_ms(reset=True)
+        r.set_profiling(False)
+        out = {k: st_[k][0] / len(views) for k in ("count", "emit", "raster", "backward")}
+        out["total"] = sum(out.values())
+        return out
+
+    variants = {}
+    side_views = my_views[:8]
+    variants["plain"] = per_view_ms(rast, d["desc"], side_views)
+    for name, kw in (("t_min_0.01", {"t_min": 0.01}), ("coarse_all_layers", {"coarse_layers": sc.n_layers - 1})):
+        rv = Rasterizer(W, H, sc.n_layers, F, max_points=n, device=dev, **kw)
+        variants[name] = per_view_ms(rv, d["desc"], side_views)
+        del rv
+    for Fv in (6, 8):
+        gen = torch.Generator(device=dev).manual_seed(Fv)
+        dv8 = (torch.randn(n, Fv, generator=gen, device=dev) * 0.5).contiguous()
+        rv = Rasterizer(W, H, sc.n_layers, Fv, max_points=n, device=dev)
+        variants[f"F{Fv}"] = per_view_ms(rv, dv8, side_views)
+        del rv, dv8
+    torch.cuda.empty_cache()
+
     # ---- side measurement: 4-NN point-size initialisation of the cloud
     from paper_2401_06003_b200 import knn_sizes
     knn_sizes(d["pos"])
@@ -369,6 +406,7 @@ def run_cuda(args, rank, world, local_rank):
         if random_order is not None:
             line["random_point_order"] = random_order
         line["backward_ms_per_view"] = cam_ms
+        line["variants_ms_per_view"] = variants
         knn = {"ms": knn_ms, "points_per_s": n / (knn_ms * 1e-3)}
         if world == 1 and not args.no_cpu_baseline:
             from oracle import oracle as _o
