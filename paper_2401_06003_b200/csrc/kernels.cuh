@@ -24,9 +24,24 @@ namespace trips {
 #ifndef TRIPS_RASTER_CTAS
 #define TRIPS_RASTER_CTAS 3
 #endif
+#ifndef TRIPS_PRELOAD
+#define TRIPS_PRELOAD 1
+#endif
+#ifndef TRIPS_BWD_SMEM_T
+#define TRIPS_BWD_SMEM_T 0
+#endif
+#ifndef TRIPS_BWD_CTAS
+#define TRIPS_BWD_CTAS 1
+#endif
+#ifndef TRIPS_BLEND_PREFETCH
+#define TRIPS_BLEND_PREFETCH 0
+#endif
 constexpr int kChunk = TRIPS_CHUNK;         // (point, tile) pairs staged per K4 iteration
 constexpr int kPairsPerThread = kChunk / kTilePix;
-constexpr int kBatch = 4;                   // record gathers issued together (memory-level parallelism)
+#ifndef TRIPS_BWD_BATCH
+#define TRIPS_BWD_BATCH 4
+#endif
+constexpr int kBatch = TRIPS_BWD_BATCH;     // record gathers issued together (memory-level parallelism)
 constexpr int kBlendBatch = TRIPS_BLEND_BATCH;  // same in k_raster's blend (register budget: 3 CTAs/SM)
 
 // Experiment builds only (-DTRIPS_PHASE_CLOCK): per-phase clock64 accumulation of k_raster
@@ -211,14 +226,31 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
         // cloud hit the same pixels, and same-address shared atomics within a warp serialise.
         uint32_t fq[kPairsPerThread][4];             // (q | rank << 8), 0xffffffff = none
         const int jl = (tid & 31) * 8 + (tid >> 5);
+#if TRIPS_PRELOAD
+        // all of this thread's pair loads issued before the first shared-memory atomic (a
+        // generic-pointer load cannot be hoisted across them); keys stay live for phase B
+        uint64_t pk[kPairsPerThread];
+        uint32_t po[kPairsPerThread];
+#pragma unroll
+        for (int k = 0; k < kPairsPerThread; ++k) {
+            const int j = jl + k * kTilePix;
+            pk[k] = j < m ? __ldg(reinterpret_cast<const unsigned long long*>(P.bin_key) + c0 + (size_t)j * nch) : 0ull;
+            po[k] = j < m ? __ldg(P.bin_orig + c0 + (size_t)j * nch) : 0u;
+        }
+#endif
 #pragma unroll
         for (int k = 0; k < kPairsPerThread; ++k) {
 #pragma unroll
             for (int c = 0; c < 4; ++c) fq[k][c] = 0xffffffffu;
             const int j = jl + k * kTilePix;
             if (j < m) {
+#if TRIPS_PRELOAD
+                const uint64_t key = pk[k];
+                const uint32_t o = po[k];
+#else
                 const uint64_t key = P.bin_key[c0 + (size_t)j * nch];
                 const uint32_t o = P.bin_orig[c0 + (size_t)j * nch];
+#endif
                 const int qx0 = (int)(o & 31u) - 1, qy0 = (int)(o >> 5) - 1;
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
@@ -251,7 +283,11 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
         for (int k = 0; k < kPairsPerThread; ++k) {
             const int j = jl + k * kTilePix;
             if (j < m) {
+#if TRIPS_PRELOAD
+                const uint64_t key = pk[k];
+#else
                 const uint64_t key = P.bin_key[c0 + (size_t)j * nch];
+#endif
 #pragma unroll
                 for (int c = 0; c < 4; ++c)
                     if (fq[k][c] != 0xffffffffu) s_keys[s_base[fq[k][c] & 0xffu] + (fq[k][c] >> 8)] = key;
@@ -347,6 +383,12 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
     // T_min variant (0 = the exact definition): the kept list ends with
     // the fragment after which the fp32 transmittance drops below t_min
     int Keff = K;
+#if TRIPS_BLEND_PREFETCH
+    // pull every kept record towards L1 before the dependent batch loop (no registers held)
+#pragma unroll
+    for (int mm = 0; mm < kCap; ++mm)
+        if (mm < K) asm volatile("prefetch.global.L1 [%0];" :: "l"(P.rec + (size_t)(uint32_t)r[mm] * P.RS));
+#endif
 #pragma unroll
     for (int b = 0; b < kCap / kBlendBatch; ++b) {
         if (b * kBlendBatch >= Keff || (!save && T == 0.f)) break;
@@ -509,7 +551,7 @@ __global__ void __launch_bounds__(kTilePix) k_coarse_blend(Params P, float* __re
 // grad_cam[17] += (dR row-major, dt, dfx, dfy, dcx, dcy, df), one block reduction per tile.
 // COARSE: kept keys are (z, i << 4 | d) and fragment m lives in layer l + d at (x >> d, y >> d).
 template <int FC, bool CAM, bool COARSE>
-__global__ void __launch_bounds__(kTilePix) k_backward(Params P, const float* __restrict__ gpyr,
+__global__ void __launch_bounds__(kTilePix, TRIPS_BWD_CTAS) k_backward(Params P, const float* __restrict__ gpyr,
                                                        float* __restrict__ grad, float* __restrict__ grad_cam)
 {
     const int t = blockIdx.x;
@@ -536,6 +578,21 @@ __global__ void __launch_bounds__(kTilePix) k_backward(Params P, const float* __
     const float gA = K > 0 ? __ldg(gp + P.F * plane) : 0.f;
 
     // T_m from the saved gamma_m (Eq. 6) -- no record gathers
+#if TRIPS_BWD_SMEM_T
+    // T_m staged in shared memory ([m][pixel], conflict-free) and gamma_m re-read from L1 in
+    // the reverse loop: 32 fewer live registers
+    __shared__ float s_T[kCap][kTilePix];
+    {
+        float T = 1.f;
+#pragma unroll
+        for (int mm = 0; mm < kCap; ++mm) {
+            if (mm < K) {
+                s_T[mm][tid] = T;
+                T = T * (1.0f - __ldg(gm + mm));
+            }
+        }
+    }
+#else
     float gam[kCap], Tm[kCap];
     float T = 1.f;
 #pragma unroll
@@ -544,6 +601,7 @@ __global__ void __launch_bounds__(kTilePix) k_backward(Params P, const float* __
         Tm[mm] = T;
         T = T * (1.0f - gam[mm]);
     }
+#endif
     // reverse replay with suffix recurrences (division-free):
     //   dL/dgamma_m = T_m (<gC, tau_m - B_m> + gA (1 - b_m)),
     //   B_{m-1} = gamma_m tau_m + (1 - gamma_m) B_m,   b_{m-1} = gamma_m + (1 - gamma_m) b_m
@@ -577,7 +635,11 @@ __global__ void __launch_bounds__(kTilePix) k_backward(Params P, const float* __
             const float z = __uint_as_float((uint32_t)(kb[u] >> 32));
             const float4 r0 = rb[u][0];
             const FragW w = frag_weights(r0, tc.l + d, P.n_layers, px >> d, py >> d);
+#if TRIPS_BWD_SMEM_T
+            const float g = __ldg(gm + mm), tm = s_T[mm][tid];
+#else
             const float g = gam[mm], tm = Tm[mm];
+#endif
             float tau[FC];
 #pragma unroll
             for (int c4 = 0; c4 < FC / 4; ++c4) {
