@@ -40,6 +40,7 @@ struct Params {
     int32_t n_layers, T;              // layers, total tiles
     float t_min;                      // T_min blend variant (0 = the exact definition)
     int32_t coarse;                   // coarse-layer inclusion depth (0 = the exact definition)
+    int32_t sched_D, sched_G, sched_S; // per-tile CTA schedule (kernels.cuh block_tile)
     LayerGeom L[kMaxLayers];
     Cam cam;
     // inputs (caller)

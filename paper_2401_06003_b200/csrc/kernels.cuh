@@ -167,6 +167,40 @@ __device__ __forceinline__ TileCoord tile_coord(const Params& P, int t)
     return c;
 }
 
+// Tile schedule of the per-tile kernels.  CTAs visit the pyramid group by group:
+// a group is one tile of layer D = sched_D with all its descendant tiles in layers D-1..0, in
+// quadtree post-order (the four children before their parent), so a point's two adjacent
+// layers are processed close in time and its record and gradient row are reused from L2
+// instead of being fetched again after a whole layer.  Layers above D follow in natural
+// order.  Slots whose tile lies outside the layer (ragged image borders) exit at once.
+__device__ __forceinline__ bool block_tile(const Params& P, int b, int& t, TileCoord& tc)
+{
+    const int D = P.sched_D;
+    const int nb = P.sched_G * P.sched_S;
+    if (D == 0 || b >= nb) {
+        t = D == 0 ? b : P.L[D + 1].tile_base + (b - nb);
+        tc = tile_coord(P, t);
+        return true;
+    }
+    const int g = b / P.sched_S;
+    int k = b - g * P.sched_S;
+    int l = D;
+    int x = g % P.L[D].tiles_x, y = g / P.L[D].tiles_x;
+#pragma unroll 1
+    while (k != ((1 << (2 * (l + 1))) - 1) / 3 - 1) {    // subtree of layer l: (4^(l+1) - 1) / 3 tiles
+        const int sc = ((1 << (2 * l)) - 1) / 3;         // child subtree size
+        const int c = k / sc;
+        k -= c * sc;
+        --l;
+        x = 2 * x + (c & 1);
+        y = 2 * y + (c >> 1);
+    }
+    if (x >= P.L[l].tiles_x || y >= P.L[l].tiles_y) return false;
+    t = P.L[l].tile_base + y * P.L[l].tiles_x + x;
+    tc.l = l; tc.tx = x; tc.ty = y;
+    return true;
+}
+
 // --------------------------------------------------------------------------- K4 raster
 
 // Dynamic shared memory of k_raster: the per-chunk fragment keys.  (Reusing it after the last
@@ -192,8 +226,9 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
     __shared__ uint64_t s_thr[kTilePix];             // per-pixel 16th smallest key so far
     __shared__ uint32_t s_warp[32];
 
-    const int t = blockIdx.x;
-    const TileCoord tc = tile_coord(P, t);
+    int t;
+    TileCoord tc;
+    if (!block_tile(P, blockIdx.x, t, tc)) return;
     const LayerGeom& G = P.L[tc.l];
     const int tid = threadIdx.x;
     const int lx = tid & (kTile - 1), ly = tid >> 4;
@@ -456,8 +491,9 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
 template <int FC>
 __global__ void __launch_bounds__(kTilePix) k_coarse_blend(Params P, float* __restrict__ pyramid, int save)
 {
-    const int t = blockIdx.x;
-    const TileCoord tc = tile_coord(P, t);
+    int t;
+    TileCoord tc;
+    if (!block_tile(P, blockIdx.x, t, tc)) return;
     const LayerGeom& G = P.L[tc.l];
     const int tid = threadIdx.x;
     const int px = tc.tx * kTile + (tid & (kTile - 1)), py = tc.ty * kTile + (tid >> 4);
@@ -554,8 +590,9 @@ template <int FC, bool CAM, bool COARSE>
 __global__ void __launch_bounds__(kTilePix, TRIPS_BWD_CTAS) k_backward(Params P, const float* __restrict__ gpyr,
                                                        float* __restrict__ grad, float* __restrict__ grad_cam)
 {
-    const int t = blockIdx.x;
-    const TileCoord tc = tile_coord(P, t);
+    int t;
+    TileCoord tc;
+    if (!block_tile(P, blockIdx.x, t, tc)) return;
     const LayerGeom& G = P.L[tc.l];
     const int tid = threadIdx.x;
     const int px = tc.tx * kTile + (tid & (kTile - 1)), py = tc.ty * kTile + (tid >> 4);

@@ -35,6 +35,7 @@ struct trips_plan {
     int32_t n_layers, F, FC, RS, G, W, H, T;
     float t_min;
     int32_t coarse;         // coarse-layer inclusion depth, clamped to n_layers - 1
+    int32_t sched_D, sched_G, sched_S, tile_grid;   // per-tile CTA schedule (block_tile)
     int64_t max_points, P, pyr_floats;
     LayerGeom L[kMaxLayers];
     uint64_t kcap;
@@ -147,6 +148,7 @@ Params make_params(const trips_plan* p, void* ws)
     P.n_layers = p->n_layers; P.T = p->T;
     P.t_min = p->t_min;
     P.coarse = p->coarse;
+    P.sched_D = p->sched_D; P.sched_G = p->sched_G; P.sched_S = p->sched_S;
     for (int l = 0; l < kMaxLayers; ++l) P.L[l] = p->L[l];
     P.cam = p->cam;
     char* b = static_cast<char*>(ws);
@@ -219,6 +221,21 @@ int trips_plan_create(const trips_config* cfg, int32_t width, int32_t height, in
     }
     p->P = pix;
     p->T = tiles;
+#ifndef TRIPS_GROUP_DEPTH
+#define TRIPS_GROUP_DEPTH 3
+#endif
+    // grouped tile schedule: one layer-D tile + its descendants per group (kernels.cuh)
+    p->sched_D = std::min(TRIPS_GROUP_DEPTH, n - 1);
+    if (p->sched_D > 0) {
+        const int D = p->sched_D;
+        p->sched_G = p->L[D].tiles_x * p->L[D].tiles_y;
+        p->sched_S = ((1 << (2 * (D + 1))) - 1) / 3;
+        const int rest = D + 1 < n ? tiles - p->L[D + 1].tile_base : 0;
+        p->tile_grid = p->sched_G * p->sched_S + rest;
+    } else {
+        p->sched_G = p->sched_S = 0;
+        p->tile_grid = tiles;
+    }
     p->pyr_floats = pix * (F + 1);
     const uint64_t kc1 = (uint64_t)tiles * kTilePix * kCap, kc2 = (uint64_t)max_points * 32;
     p->kcap = (p->coarse || kc1 < kc2) ? kc1 : kc2;    // coarse inclusion: dense 16 per pixel
@@ -341,13 +358,13 @@ int trips_splat_forward(trips_plan* p, void* ws, float* pyramid, uint32_t flags,
             rattr[mode][p->FC / 4] = true;
         }
         if (mode == kRasterOwn) {
-            TRIPS_FC_SWITCH(p->FC, (k_raster<kFC, kRasterOwn><<<p->T, kTilePix, rsm, st>>>(P, pyramid, save)));
+            TRIPS_FC_SWITCH(p->FC, (k_raster<kFC, kRasterOwn><<<p->tile_grid, kTilePix, rsm, st>>>(P, pyramid, save)));
             if ((rc = check_launch())) return rc;
-            TRIPS_FC_SWITCH(p->FC, (k_coarse_blend<kFC><<<p->T, kTilePix, 0, st>>>(P, pyramid, save)));
+            TRIPS_FC_SWITCH(p->FC, (k_coarse_blend<kFC><<<p->tile_grid, kTilePix, 0, st>>>(P, pyramid, save)));
         } else if (mode == kRasterTmin) {
-            TRIPS_FC_SWITCH(p->FC, (k_raster<kFC, kRasterTmin><<<p->T, kTilePix, rsm, st>>>(P, pyramid, save)));
+            TRIPS_FC_SWITCH(p->FC, (k_raster<kFC, kRasterTmin><<<p->tile_grid, kTilePix, rsm, st>>>(P, pyramid, save)));
         } else {
-            TRIPS_FC_SWITCH(p->FC, (k_raster<kFC, kRasterPlain><<<p->T, kTilePix, rsm, st>>>(P, pyramid, save)));
+            TRIPS_FC_SWITCH(p->FC, (k_raster<kFC, kRasterPlain><<<p->tile_grid, kTilePix, rsm, st>>>(P, pyramid, save)));
         }
         if ((rc = check_launch())) return rc;
     }
@@ -367,16 +384,16 @@ int trips_splat_backward(trips_plan* p, void* ws, const float* grad_pyramid, flo
     {
         StageScope sc(p, 4, st);
         if (grad_camera && p->coarse) {
-            TRIPS_FC_SWITCH(p->FC, (k_backward<kFC, true, true><<<p->T, kTilePix, 0, st>>>(P, grad_pyramid, grad,
+            TRIPS_FC_SWITCH(p->FC, (k_backward<kFC, true, true><<<p->tile_grid, kTilePix, 0, st>>>(P, grad_pyramid, grad,
                                                                                              grad_camera)));
         } else if (grad_camera) {
-            TRIPS_FC_SWITCH(p->FC, (k_backward<kFC, true, false><<<p->T, kTilePix, 0, st>>>(P, grad_pyramid, grad,
+            TRIPS_FC_SWITCH(p->FC, (k_backward<kFC, true, false><<<p->tile_grid, kTilePix, 0, st>>>(P, grad_pyramid, grad,
                                                                                               grad_camera)));
         } else if (p->coarse) {
-            TRIPS_FC_SWITCH(p->FC, (k_backward<kFC, false, true><<<p->T, kTilePix, 0, st>>>(P, grad_pyramid, grad,
+            TRIPS_FC_SWITCH(p->FC, (k_backward<kFC, false, true><<<p->tile_grid, kTilePix, 0, st>>>(P, grad_pyramid, grad,
                                                                                               nullptr)));
         } else {
-            TRIPS_FC_SWITCH(p->FC, (k_backward<kFC, false, false><<<p->T, kTilePix, 0, st>>>(P, grad_pyramid, grad,
+            TRIPS_FC_SWITCH(p->FC, (k_backward<kFC, false, false><<<p->tile_grid, kTilePix, 0, st>>>(P, grad_pyramid, grad,
                                                                                                nullptr)));
         }
         if ((rc = check_launch())) return rc;

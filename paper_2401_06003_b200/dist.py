@@ -36,6 +36,40 @@ def cuda_view_renderer(rast, cams, pos, world_size, opacity, desc, grad_pyramid)
     return render_view
 
 
+def cuda_batch_step(rasts, cams, pos, world_size, opacity, desc, grad_pyramid, views, grad, world=1, group=None,
+                    zero=True, streams=None):
+    """batch_step on the CUDA path with the views spread round-robin over len(rasts) CUDA
+    streams, one Rasterizer (plan + workspace) per stream, so that one view's memory-streaming
+    binning kernels overlap another view's latency-bound raster/backward kernels.  Gradients
+    of all views accumulate into `grad` (vector reductions are atomic, so concurrent backward
+    passes are safe); the streams join the current stream before the all-reduce."""
+    main = torch.cuda.current_stream()
+    if streams is None:
+        streams = [main] + [torch.cuda.Stream(device=grad.device) for _ in range(len(rasts) - 1)]
+    if zero:
+        grad.zero_()
+    start = torch.cuda.Event()
+    start.record(main)
+    for s in streams:
+        if s != main:
+            s.wait_event(start)
+    for j, v in enumerate(views):
+        k = j % len(rasts)
+        with torch.cuda.stream(streams[k]):
+            r = rasts[k]
+            r.project(cams[v], pos, world_size, opacity, desc)
+            r.forward(save=True)
+            r.backward(grad_pyramid(v) if callable(grad_pyramid) else grad_pyramid, grad)
+    for s in streams:
+        if s != main:
+            e = torch.cuda.Event()
+            e.record(s)
+            main.wait_event(e)
+    if world > 1:
+        dist.all_reduce(grad, op=dist.ReduceOp.SUM, group=group)
+    return grad
+
+
 def init_from_env(backend=None):
     """torch.distributed init from torchrun's env (RANK, WORLD_SIZE, LOCAL_RANK, MASTER_*).
     Returns (rank, world, local_rank); world == 1 without a launcher."""
