@@ -222,7 +222,7 @@ int trips_plan_create(const trips_config* cfg, int32_t width, int32_t height, in
     p->P = pix;
     p->T = tiles;
 #ifndef TRIPS_GROUP_DEPTH
-#define TRIPS_GROUP_DEPTH 3
+#define TRIPS_GROUP_DEPTH 0
 #endif
     // grouped tile schedule: one layer-D tile + its descendants per group (kernels.cuh)
     p->sched_D = std::min(TRIPS_GROUP_DEPTH, n - 1);

@@ -217,6 +217,29 @@ def test_multi_view_accumulation(dev):
     assert np.all(np.abs(got - acc) <= GRAD_TOL * accm + 1e-30)
 
 
+def test_batch_step_over_two_streams(dev):
+    """dist.cuda_batch_step: views spread over 2 streams / 2 workspaces accumulate the same
+    gradient sum as the oracle (reading Q21), concurrent reductions included."""
+    from paper_2401_06003_b200 import Rasterizer
+    from paper_2401_06003_b200 import dist as tdist
+    sc = scenes.make_config("C4", n=20000, n_views=5)
+    cams = [scenes.look_at(-c.R.T.astype(np.float64) @ c.t.astype(np.float64), [0, 0, 0], 160, 96, 100.0)
+            for c in sc.cams]
+    rasts = [Rasterizer(160, 96, 4, sc.F, max_points=sc.n, device=dev) for _ in range(2)]
+    pos, sw, al, de = (T(a, dev) for a in (sc.pos, sc.sw, sc.alpha, sc.desc))
+    Gs = [scenes.grad_pyramid(rasts[0].pyramid_floats, seed=v) for v in range(5)]
+    Gd = [T(g, dev) for g in Gs]
+    grad = torch.full((sc.n, rasts[0].G), 7.0, device=dev)            # zeroed by the step
+    tdist.cuda_batch_step(rasts, cams, pos, sw, al, de, lambda v: Gd[v], range(5), grad)
+    torch.cuda.synchronize()
+    acc, accm = None, None
+    for v, cam in enumerate(cams):
+        acc, accm = oracle.backward(cam, 4, sc.pos, sc.sw, sc.alpha, sc.desc, Gs[v], grad=acc, grad_mag=accm)
+    gg = grad.cpu().numpy()
+    got = np.concatenate([gg[:, :5], gg[:, 5:5 + sc.F]], 1)
+    assert np.all(np.abs(got - acc) <= GRAD_TOL * accm + 1e-30)
+
+
 def test_autograd_render(dev):
     from paper_2401_06003_b200 import Rasterizer
     sc = scenes.c1()
