@@ -108,6 +108,9 @@ __global__ void __launch_bounds__(kBinThreads) k_count(Params P, int8_t* __restr
         const bool vis = project_exact(P.cam, in[u][0], in[u][1], in[u][2], in[u][3], xs, ys, z, s);
         float4* r = reinterpret_cast<float4*>(P.rec + (size_t)i * P.RS);
         r[0] = make_float4(vis ? xs : 0.f, vis ? ys : 0.f, vis ? s : kCulled, in[u][4]);
+#if TRIPS_SPLIT_REC
+        r = reinterpret_cast<float4*>(P.tau + (size_t)i * FC) - 1;     // r[1 + c] = tau block c
+#endif
         const float* d = P.desc + (size_t)i * P.F;
         if (vec_desc) {
 #pragma unroll

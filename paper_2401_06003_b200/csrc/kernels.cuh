@@ -31,7 +31,7 @@ namespace trips {
 #define TRIPS_BWD_SMEM_T 0
 #endif
 #ifndef TRIPS_BWD_CTAS
-#define TRIPS_BWD_CTAS 1
+#define TRIPS_BWD_CTAS 3
 #endif
 #ifndef TRIPS_BLEND_PREFETCH
 #define TRIPS_BLEND_PREFETCH 0
@@ -173,8 +173,16 @@ __device__ __forceinline__ TileCoord tile_coord(const Params& P, int t)
 // layers are processed close in time and its record and gradient row are reused from L2
 // instead of being fetched again after a whole layer.  Layers above D follow in natural
 // order.  Slots whose tile lies outside the layer (ragged image borders) exit at once.
+#ifndef TRIPS_GROUP_DEPTH
+#define TRIPS_GROUP_DEPTH 0     // measured slower than the natural order (profiles/r01_v2.md)
+#endif
 __device__ __forceinline__ bool block_tile(const Params& P, int b, int& t, TileCoord& tc)
 {
+#if TRIPS_GROUP_DEPTH == 0
+    t = b;
+    tc = tile_coord(P, t);
+    return true;
+#endif
     const int D = P.sched_D;
     const int nb = P.sched_G * P.sched_S;
     if (D == 0 || b >= nb) {
@@ -410,7 +418,6 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
     const uint32_t koff = block_excl_scan((uint32_t)K, s_warp, &ktot);
     TRIPS_PCLK(4);
     const size_t kidx = (size_t)P.tile_kbase[t] + koff;
-    constexpr int kR4 = 1 + FC / 4;                  // float4s per point record
     float C[FC];
 #pragma unroll
     for (int c = 0; c < FC; ++c) C[c] = 0.f;
@@ -432,9 +439,7 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
         for (int u = 0; u < kBlendBatch; ++u) {
             const int mm = b * kBlendBatch + u;                  // compile-time register index
             const uint32_t ii = (uint32_t)(mm < K ? r[mm] : r[0]);
-            const float4* rp = reinterpret_cast<const float4*>(P.rec + (size_t)ii * P.RS);
-#pragma unroll
-            for (int c4 = 0; c4 < kR4; ++c4) rb[u][c4] = __ldg(rp + c4);
+            gather_record<FC>(P, ii, rb[u]);
         }
 #pragma unroll
         for (int u = 0; u < kBlendBatch; ++u) {
@@ -524,7 +529,6 @@ __global__ void __launch_bounds__(kTilePix) k_coarse_blend(Params P, float* __re
     K = min(K, kCap);
 
     const size_t kidx = (size_t)P.tile_kbase[t] + (size_t)tid * kCap;
-    constexpr int kR4 = 1 + FC / 4;
     float C[FC];
 #pragma unroll
     for (int c = 0; c < FC; ++c) C[c] = 0.f;
@@ -538,9 +542,7 @@ __global__ void __launch_bounds__(kTilePix) k_coarse_blend(Params P, float* __re
         for (int u = 0; u < kBlendBatch; ++u) {
             const int mm = b * kBlendBatch + u;
             const uint32_t ii = (uint32_t)(mm < K ? r[mm] : r[0]) >> 4;
-            const float4* rp = reinterpret_cast<const float4*>(P.rec + (size_t)ii * P.RS);
-#pragma unroll
-            for (int c4 = 0; c4 < kR4; ++c4) rb[u][c4] = __ldg(rp + c4);
+            gather_record<FC>(P, ii, rb[u]);
         }
 #pragma unroll
         for (int u = 0; u < kBlendBatch; ++u) {
@@ -658,9 +660,7 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_BWD_CTAS) k_backward(Params P,
             const int mm = min(b * kBatch + u, K - 1);
             kb[u] = __ldg(reinterpret_cast<const unsigned long long*>(kp) + mm);
             const uint32_t iu = COARSE ? (uint32_t)kb[u] >> 4 : (uint32_t)kb[u];
-            const float4* rp = reinterpret_cast<const float4*>(P.rec + (size_t)iu * P.RS);
-#pragma unroll
-            for (int c4 = 0; c4 <= FC / 4; ++c4) rb[u][c4] = __ldg(rp + c4);
+            gather_record<FC>(P, iu, rb[u]);
         }
 #pragma unroll
         for (int u = kBatch - 1; u >= 0; --u) {

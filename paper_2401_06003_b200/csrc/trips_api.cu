@@ -42,7 +42,7 @@ struct trips_plan {
     // workspace layout (byte offsets)
     int32_t ctas;           // binning CTAs (persistent grid)
     size_t off_rec, off_z, off_hist, off_cvis, off_toff, off_tkb, off_bkey, off_borig, off_pcnt, off_pmeta, off_kept, off_kgam,
-        off_own, off_stats, ws_bytes;
+        off_own, off_tau, off_stats, ws_bytes;
     // state
     const void* ws_bound = nullptr;
     int stage = 0;          // 0 none, 1 projected, 2 forward (saved), 3 forward (not saved)
@@ -154,6 +154,7 @@ Params make_params(const trips_plan* p, void* ws)
     char* b = static_cast<char*>(ws);
     P.rec = reinterpret_cast<float*>(b + p->off_rec);
     P.zbuf = reinterpret_cast<float*>(b + p->off_z);
+    P.tau = reinterpret_cast<float*>(b + p->off_tau);
     P.hist = reinterpret_cast<uint32_t*>(b + p->off_hist);
     P.cta_vis = reinterpret_cast<uint32_t*>(b + p->off_cvis);
     P.tile_off = reinterpret_cast<uint32_t*>(b + p->off_toff);
@@ -200,7 +201,7 @@ int trips_plan_create(const trips_config* cfg, int32_t width, int32_t height, in
     if (width < 1 || height < 1 || width > 32768 || height > 32768) return TRIPS_ERR_ARG;
     if (max_points < 0 || max_points >= (int64_t(1) << 28)) return TRIPS_ERR_ARG;
     trips_plan* p = new trips_plan();
-    p->n_layers = n; p->F = F; p->FC = (F + 3) & ~3; p->RS = 4 + p->FC; p->G = 8 + p->FC;
+    p->n_layers = n; p->F = F; p->FC = (F + 3) & ~3; p->RS = TRIPS_SPLIT_REC ? 4 : 4 + p->FC; p->G = 8 + p->FC;
     p->t_min = cfg->t_min;
     p->coarse = std::min(cfg->coarse_layers, n - 1);
     p->W = width; p->H = height; p->max_points = max_points;
@@ -221,9 +222,6 @@ int trips_plan_create(const trips_config* cfg, int32_t width, int32_t height, in
     }
     p->P = pix;
     p->T = tiles;
-#ifndef TRIPS_GROUP_DEPTH
-#define TRIPS_GROUP_DEPTH 0
-#endif
     // grouped tile schedule: one layer-D tile + its descendants per group (kernels.cuh)
     p->sched_D = std::min(TRIPS_GROUP_DEPTH, n - 1);
     if (p->sched_D > 0) {
@@ -245,6 +243,7 @@ int trips_plan_create(const trips_config* cfg, int32_t width, int32_t height, in
     p->ctas = num_sms() * kBinCtasPerSm;
     p->off_rec = o;    o = align256(o + N * p->RS * sizeof(float));
     p->off_z = o;      o = align256(o + N * sizeof(float));
+    p->off_tau = o;    o = align256(o + (TRIPS_SPLIT_REC ? N * p->FC * sizeof(float) : 0));
     p->off_hist = o;   o = align256(o + (size_t)p->ctas * tiles * 4);
     p->off_cvis = o;   o = align256(o + (size_t)p->ctas * 4);
     p->off_toff = o;   o = align256(o + ((size_t)tiles + 1) * 4);
