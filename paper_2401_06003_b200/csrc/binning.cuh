@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(1024) k_tscan(Params P)
 
 // Same point partition as k_count: re-enumerates each visible point's pairs from its screen
 // record (no projection) and places them at tile_off[t] + this CTA's slice + shared cursor.
-__global__ void __launch_bounds__(kBinThreads) k_emit(Params P)
+__global__ void __launch_bounds__(kBinThreads, kBinCtasPerSm) k_emit(Params P)
 {
     extern __shared__ __align__(16) uint32_t s_cur[];             // [T] fill cursors
     const uint32_t* row = P.hist + (size_t)blockIdx.x * P.T;
@@ -202,15 +202,30 @@ __global__ void __launch_bounds__(kBinThreads) k_emit(Params P)
     __syncthreads();
     int b, e;
     cta_range(P.n, b, e);
-    for (int i = b + threadIdx.x; i < e; i += blockDim.x) {
-        const float4 r0 = __ldg(reinterpret_cast<const float4*>(P.rec + (size_t)i * P.RS));
-        if (!(r0.z >= 0.f)) continue;                             // culled
-        const uint64_t key = ((uint64_t)__float_as_uint(__ldg(P.zbuf + i)) << 32) | (uint32_t)i;
-        for_each_pair(P, r0.x, r0.y, r0.z, [&](int t, uint32_t o) {
-            const uint32_t pos = atomicAdd(&s_cur[t], 1u);
-            P.bin_key[pos] = key;
-            P.bin_orig[pos] = (uint16_t)o;
-        });
+#ifndef TRIPS_EMIT_UNROLL
+#define TRIPS_EMIT_UNROLL 1
+#endif
+    constexpr int kU = TRIPS_EMIT_UNROLL;         // points per thread per iteration (loads issued together)
+    for (int i0 = b + threadIdx.x; i0 < e; i0 += kU * blockDim.x) {
+        float4 r0[kU];
+        float zz[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int i = min(i0 + u * (int)blockDim.x, e - 1);
+            r0[u] = __ldg(reinterpret_cast<const float4*>(P.rec + (size_t)i * P.RS));
+            zz[u] = __ldg(P.zbuf + i);
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int i = i0 + u * (int)blockDim.x;
+            if (i >= e || !(r0[u].z >= 0.f)) continue;            // past the range / culled
+            const uint64_t key = ((uint64_t)__float_as_uint(zz[u]) << 32) | (uint32_t)i;
+            for_each_pair(P, r0[u].x, r0[u].y, r0[u].z, [&](int t, uint32_t o) {
+                const uint32_t pos = atomicAdd(&s_cur[t], 1u);
+                P.bin_key[pos] = key;
+                P.bin_orig[pos] = (uint16_t)o;
+            });
+        }
     }
 }
 
