@@ -585,11 +585,56 @@ __global__ void __launch_bounds__(kTilePix) k_coarse_blend(Params P, float* __re
 
 // --------------------------------------------------------------------------- K5 backward
 
-// CAM: also accumulate the camera gradient:
-// grad_cam[17] += (dR row-major, dt, dfx, dfy, dcx, dcy, df), one block reduction per tile.
-// COARSE: kept keys are (z, i << 4 | d) and fragment m lives in layer l + d at (x >> d, y >> d).
+// Screen-space gradient of one point (gxs, gys, gs: d/dx, d/dy, d/ds in image pixels; galpha;
+// gtau[F]) -> world space through the projection chain (Eq. 2, Sec. 3.1), reduced into its
+// packed row with 16-byte vector reductions; CAM: camera partials into cg.
+template <int FC, bool CAM>
+__device__ __forceinline__ void point_reduce(const Params& P, uint32_t i, float4 r0, float z, float gxs, float gys,
+                                             float gs, float galpha, const float (&gtau)[FC], float* __restrict__ grad,
+                                             float (&cg)[CAM ? 17 : 1])
+{
+    const Cam& cam = P.cam;
+    const float iz = 1.0f / z;
+    const float gpx = gxs * cam.fx * iz, gpy = gys * cam.fy * iz;
+    const float gpz = -(gxs * (r0.x - cam.cx) + gys * (r0.y - cam.cy) + gs * r0.z) * iz;
+    const float gX = cam.R[0] * gpx + cam.R[3] * gpy + cam.R[6] * gpz;
+    const float gY = cam.R[1] * gpx + cam.R[4] * gpy + cam.R[7] * gpz;
+    const float gZ = cam.R[2] * gpx + cam.R[5] * gpy + cam.R[8] * gpz;
+    const float gsw = gs * cam.f * iz;
+    if (CAM) {
+        // p = (px, py, z) from the screen record, X = R^T (p - t)
+        const float pxv = (r0.x - cam.cx) * z / cam.fx, pyv = (r0.y - cam.cy) * z / cam.fy;
+        const float q0 = pxv - cam.t[0], q1 = pyv - cam.t[1], q2 = z - cam.t[2];
+        const float Xw[3] = {cam.R[0] * q0 + cam.R[3] * q1 + cam.R[6] * q2,
+                             cam.R[1] * q0 + cam.R[4] * q1 + cam.R[7] * q2,
+                             cam.R[2] * q0 + cam.R[5] * q1 + cam.R[8] * q2};
+        const float gpv[3] = {gpx, gpy, gpz};
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+#pragma unroll
+            for (int b = 0; b < 3; ++b) cg[3 * a + b] = fmaf(gpv[a], Xw[b], cg[3 * a + b]);
+            cg[9 + a] += gpv[a];
+        }
+        cg[12] = fmaf(gxs, pxv * iz, cg[12]);
+        cg[13] = fmaf(gys, pyv * iz, cg[13]);
+        cg[14] += gxs;
+        cg[15] += gys;
+        cg[16] = fmaf(gs, r0.z / cam.f, cg[16]);
+    }
+    float* grow = grad + (size_t)i * P.G;
+    red_add_v4(grow, gX, gY, gZ, gsw);
+    float v[FC + 4];
+    v[0] = galpha;
+#pragma unroll
+    for (int c = 0; c < FC; ++c) v[1 + c] = gtau[c];
+    v[FC + 1] = 0.f; v[FC + 2] = 0.f; v[FC + 3] = 0.f;
+#pragma unroll
+    for (int c4 = 0; c4 < (FC + 4) / 4; ++c4)
+        if (4 * c4 < P.F + 1) red_add_v4(grow + 4 + 4 * c4, v[4 * c4], v[4 * c4 + 1], v[4 * c4 + 2], v[4 * c4 + 3]);
+}
+
 template <int FC, bool CAM, bool COARSE>
-__global__ void __launch_bounds__(kTilePix, TRIPS_BWD_CTAS) k_backward(Params P, const float* __restrict__ gpyr,
+__global__ void __launch_bounds__(kTilePix, FC <= 4 ? TRIPS_BWD_CTAS : 2) k_backward(Params P, const float* __restrict__ gpyr,
                                                        float* __restrict__ grad, float* __restrict__ grad_cam)
 {
     int t;
@@ -649,7 +694,6 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_BWD_CTAS) k_backward(Params P,
     for (int c = 0; c < FC; ++c) B[c] = 0.f;
     float bb = 0.f;
     const float sc0 = pow2_neg(tc.l);
-    const Cam& cam = P.cam;
 #pragma unroll
     for (int b = kCap / kBatch - 1; b >= 0; --b) {
         if (b * kBatch >= K) continue;
@@ -694,44 +738,10 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_BWD_CTAS) k_backward(Params P,
             const float gxs = gbeta * w.wy * (w.dx ? 1.f : -1.f) * sc;
             const float gys = gbeta * w.wx * (w.dy ? 1.f : -1.f) * sc;
             const float gs = giota * w.diota;
-            // projection chain (Eq. 2, Sec. 3.1)
-            const float iz = 1.0f / z;
-            const float gpx = gxs * cam.fx * iz, gpy = gys * cam.fy * iz;
-            const float gpz = -(gxs * (r0.x - cam.cx) + gys * (r0.y - cam.cy) + gs * r0.z) * iz;
-            const float gX = cam.R[0] * gpx + cam.R[3] * gpy + cam.R[6] * gpz;
-            const float gY = cam.R[1] * gpx + cam.R[4] * gpy + cam.R[7] * gpz;
-            const float gZ = cam.R[2] * gpx + cam.R[5] * gpy + cam.R[8] * gpz;
-            const float gsw = gs * cam.f * iz;
-            if (CAM) {
-                // p = (px, py, z) from the screen record, X = R^T (p - t)
-                const float pxv = (r0.x - cam.cx) * z / cam.fx, pyv = (r0.y - cam.cy) * z / cam.fy;
-                const float q0 = pxv - cam.t[0], q1 = pyv - cam.t[1], q2 = z - cam.t[2];
-                const float Xw[3] = {cam.R[0] * q0 + cam.R[3] * q1 + cam.R[6] * q2,
-                                     cam.R[1] * q0 + cam.R[4] * q1 + cam.R[7] * q2,
-                                     cam.R[2] * q0 + cam.R[5] * q1 + cam.R[8] * q2};
-                const float gpv[3] = {gpx, gpy, gpz};
+            float gt[FC];
 #pragma unroll
-                for (int a = 0; a < 3; ++a) {
-#pragma unroll
-                    for (int bb2 = 0; bb2 < 3; ++bb2) cg[3 * a + bb2] = fmaf(gpv[a], Xw[bb2], cg[3 * a + bb2]);
-                    cg[9 + a] += gpv[a];
-                }
-                cg[12] = fmaf(gxs, pxv * iz, cg[12]);
-                cg[13] = fmaf(gys, pyv * iz, cg[13]);
-                cg[14] += gxs;
-                cg[15] += gys;
-                cg[16] = fmaf(gs, r0.z / cam.f, cg[16]);
-            }
-            float* grow = grad + (size_t)i * P.G;
-            red_add_v4(grow, gX, gY, gZ, gsw);
-            float v[FC + 4];
-            v[0] = galpha;
-#pragma unroll
-            for (int c = 0; c < FC; ++c) v[1 + c] = tg * gC[c];
-            v[FC + 1] = 0.f; v[FC + 2] = 0.f; v[FC + 3] = 0.f;
-#pragma unroll
-            for (int c4 = 0; c4 < (FC + 4) / 4; ++c4)
-                if (4 * c4 < P.F + 1) red_add_v4(grow + 4 + 4 * c4, v[4 * c4], v[4 * c4 + 1], v[4 * c4 + 2], v[4 * c4 + 3]);
+            for (int c = 0; c < FC; ++c) gt[c] = tg * gC[c];
+            point_reduce<FC, CAM>(P, i, r0, z, gxs, gys, gs, galpha, gt, grad, cg);
 #pragma unroll
             for (int c = 0; c < FC; ++c) B[c] = g * tau[c] + (1.0f - g) * B[c];
             bb = g + (1.0f - g) * bb;
