@@ -70,6 +70,53 @@ def cuda_batch_step(rasts, cams, pos, world_size, opacity, desc, grad_pyramid, v
     return grad
 
 
+class StreamedSteps:
+    """End-to-end step pipeline from pinned host memory: every step copies its inputs host ->
+    device, runs `step_fn(device_inputs, grad)` and copies the gradient buffer device -> host.
+    Inputs and gradients are double-buffered and the copies run on their own streams, so step
+    k+1's upload and step k-1's download overlap step k's kernels (the copy engines are
+    separate from the SMs); event edges keep every buffer reuse ordered.
+
+        pipe = StreamedSteps(host_inputs, grad_like, device)
+        pipe.run(steps, step_fn, host_out)        # host_out[k % 2] holds step k's gradients
+    """
+
+    def __init__(self, host_inputs, grad_like, device):
+        self.host = host_inputs
+        self.dev_in = [{k: torch.empty_like(v, device=device) for k, v in host_inputs.items()} for _ in range(2)]
+        self.grads = [grad_like, torch.empty_like(grad_like)]
+        self.up = torch.cuda.Stream(device=device)
+        self.down = torch.cuda.Stream(device=device)
+
+    def run(self, steps, step_fn, host_out):
+        main = torch.cuda.current_stream()
+        done = [None, None]      # compute of the step that last used buffer b finished
+        out = [None, None]       # download of gradient buffer b finished
+        for k in range(steps):
+            b = k % 2
+            with torch.cuda.stream(self.up):
+                if done[b] is not None:
+                    self.up.wait_event(done[b])
+                for key, v in self.host.items():
+                    self.dev_in[b][key].copy_(v, non_blocking=True)
+                ready = torch.cuda.Event()
+                ready.record(self.up)
+            main.wait_event(ready)
+            if out[b] is not None:
+                main.wait_event(out[b])
+            step_fn(self.dev_in[b], self.grads[b])
+            done[b] = torch.cuda.Event()
+            done[b].record(main)
+            with torch.cuda.stream(self.down):
+                self.down.wait_event(done[b])
+                host_out[b].copy_(self.grads[b], non_blocking=True)
+                out[b] = torch.cuda.Event()
+                out[b].record(self.down)
+        for e in out:
+            if e is not None:
+                main.wait_event(e)
+
+
 def init_from_env(backend=None):
     """torch.distributed init from torchrun's env (RANK, WORLD_SIZE, LOCAL_RANK, MASTER_*).
     Returns (rank, world, local_rank); world == 1 without a launcher."""

@@ -240,6 +240,35 @@ def test_batch_step_over_two_streams(dev):
     assert np.all(np.abs(got - acc) <= GRAD_TOL * accm + 1e-30)
 
 
+def test_streamed_steps_pipeline(dev):
+    """dist.StreamedSteps: double-buffered host->device->host steps give every step's exact
+    gradients (same as a synchronous step) in host memory."""
+    from paper_2401_06003_b200 import Rasterizer
+    from paper_2401_06003_b200 import dist as tdist
+    sc = scenes.make_config("C4", n=20000, n_views=3)
+    cams = [scenes.look_at(-c.R.T.astype(np.float64) @ c.t.astype(np.float64), [0, 0, 0], 160, 96, 100.0)
+            for c in sc.cams]
+    rasts = [Rasterizer(160, 96, 4, sc.F, max_points=sc.n, device=dev) for _ in range(2)]
+    G = T(scenes.grad_pyramid(rasts[0].pyramid_floats, seed=3), dev)
+    host = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory()
+            for k, v in (("pos", sc.pos), ("sw", sc.sw), ("alpha", sc.alpha), ("desc", sc.desc))}
+
+    def step(dv, g):
+        tdist.cuda_batch_step(rasts, cams, dv["pos"], dv["sw"], dv["alpha"], dv["desc"], G, range(3), g)
+
+    ref = torch.zeros(sc.n, rasts[0].G, device=dev)
+    step({k: v.to(dev) for k, v in host.items()}, ref)
+    torch.cuda.synchronize()
+    ref = ref.cpu().numpy()
+    out = [torch.zeros(sc.n, rasts[0].G).pin_memory() for _ in range(2)]
+    pipe = tdist.StreamedSteps(host, torch.zeros(sc.n, rasts[0].G, device=dev), dev)
+    pipe.run(5, step, out)
+    torch.cuda.synchronize()
+    for o in out:
+        got = o.numpy()
+        assert np.allclose(got, ref, rtol=1e-5, atol=1e-6 * np.abs(ref).max())
+
+
 def test_autograd_render(dev):
     from paper_2401_06003_b200 import Rasterizer
     sc = scenes.c1()
