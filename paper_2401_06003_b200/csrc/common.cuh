@@ -213,7 +213,10 @@ __device__ __forceinline__ int pair_slot(const Params& P, const PointPairs& pp, 
 
 // Calls fn(tile, orig) for every (point, tile) pair of a point (same pairs as the slot form
 // above, without evaluating empty slots): per selected layer, the tiles touched by the
-// in-bounds pixels of the 2x2 footprint; orig = footprint origin relative to the tile.
+// in-bounds pixels of the 2x2 footprint; orig = footprint origin relative to the tile
+// ((qx0 + 1) | (qy0 + 1) << 5) and, in bits 10-13, which of the 4 corners (c = dx + 2 dy) are
+// pixels of this tile inside the layer -- computed here, in the memory-bound binning pass,
+// instead of per pair in the ALU-bound raster kernel.
 template <class Fn>
 __device__ __forceinline__ void for_each_pair(const Params& P, float xs, float ys, float s, Fn&& fn)
 {
@@ -227,9 +230,16 @@ __device__ __forceinline__ void for_each_pair(const Params& P, float xs, float y
         const int ya = max(f.y0, 0), yb = min(f.y0 + 1, G.H - 1);
         if (xa > xb || ya > yb) continue;
         for (int ty = ya >> 4; ty <= (yb >> 4); ++ty)
-            for (int tx = xa >> 4; tx <= (xb >> 4); ++tx)
+            for (int tx = xa >> 4; tx <= (xb >> 4); ++tx) {
+                // columns / rows of the footprint inside [xa, xb] and this tile (separable)
+                const int cxa = max(xa, tx * 16), cxb = min(xb, tx * 16 + 15);
+                const int cya = max(ya, ty * 16), cyb = min(yb, ty * 16 + 15);
+                const uint32_t vx = (f.x0 >= cxa ? 1u : 0u) | (f.x0 + 1 <= cxb ? 2u : 0u);
+                const uint32_t vy = (f.y0 >= cya ? 1u : 0u) | (f.y0 + 1 <= cyb ? 2u : 0u);
+                const uint32_t cm = ((vy & 1u) ? vx : 0u) | ((vy & 2u) ? vx << 2 : 0u);
                 fn(G.tile_base + ty * G.tiles_x + tx,
-                   (uint32_t)(f.x0 - tx * 16 + 1) | ((uint32_t)(f.y0 - ty * 16 + 1) << 5));
+                   (uint32_t)(f.x0 - tx * 16 + 1) | ((uint32_t)(f.y0 - ty * 16 + 1) << 5) | (cm << 10));
+            }
     }
 }
 

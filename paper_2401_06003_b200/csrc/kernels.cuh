@@ -294,12 +294,11 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
                 const uint64_t key = P.bin_key[c0 + (size_t)j * nch];
                 const uint32_t o = P.bin_orig[c0 + (size_t)j * nch];
 #endif
-                const int qx0 = (int)(o & 31u) - 1, qy0 = (int)(o >> 5) - 1;
+                const int q0 = (int)(o & 31u) - 1 + ((int)((o >> 5) & 31u) - 1) * kTile;   // may be < 0
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
-                    const int qx = qx0 + (c & 1), qy = qy0 + (c >> 1);
-                    if (qx >= 0 && qx < kTile && qy >= 0 && qy < kTile && x_lo + qx < G.W && y_lo + qy < G.H) {
-                        const uint32_t q = (uint32_t)(qy * kTile + qx);
+                    if (o & (1u << (10 + c))) {               // corner inside this tile and layer
+                        const uint32_t q = (uint32_t)(q0 + (c & 1) + (c >> 1) * kTile);
                         if (key >= s_thr[q]) {
                             // cannot enter this pixel's top-16 any more (keys are unique):
                             // counted for the list length, never sorted
