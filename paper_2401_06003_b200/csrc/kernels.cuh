@@ -340,32 +340,6 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
         // phase C: merge this pixel's new fragments into its running top-16.  Network sizes are
         // chosen per warp (8 when no lane of the warp has more than 8 keys left in the group).
         const uint32_t wcnt = __reduce_max_sync(0xffffffffu, my_cnt);
-#ifdef TRIPS_GROUP8
-        // 8-key groups only: fewer live registers (4 CTAs/SM), slightly more comparators
-        for (uint32_t g = 0; g < wcnt; g += 8) {
-            const uint32_t rem = my_cnt > g ? my_cnt - g : 0u;
-            const bool first = __all_sync(0xffffffffu, total == 0 && g == 0);
-            uint64_t t8[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) t8[j] = ((uint32_t)j < rem) ? s_keys[my_base + g + j] : kKeyMax;
-            cswap(t8[0], t8[1]); cswap(t8[2], t8[3]); cswap(t8[0], t8[2]); cswap(t8[1], t8[3]); cswap(t8[1], t8[2]);
-            cswap(t8[4], t8[5]); cswap(t8[6], t8[7]); cswap(t8[4], t8[6]); cswap(t8[5], t8[7]); cswap(t8[5], t8[6]);
-            cswap(t8[0], t8[4]); cswap(t8[2], t8[6]); cswap(t8[2], t8[4]); cswap(t8[1], t8[5]); cswap(t8[3], t8[7]);
-            cswap(t8[3], t8[5]); cswap(t8[1], t8[2]); cswap(t8[3], t8[4]); cswap(t8[5], t8[6]);
-            if (first) {
-#pragma unroll
-                for (int j = 0; j < 8; ++j) r[j] = t8[j];
-            } else {
-#pragma unroll
-                for (int j = 8; j < 16; ++j) r[j] = r[j] < t8[15 - j] ? r[j] : t8[15 - j];
-#pragma unroll
-                for (int d = 8; d > 0; d >>= 1)
-#pragma unroll
-                    for (int i = 0; i < 16; ++i)
-                        if ((i & d) == 0) cswap(r[i], r[i + d]);
-            }
-        }
-#else
         for (uint32_t g = 0; g < wcnt; g += 16) {
             const uint32_t rem = my_cnt > g ? my_cnt - g : 0u;
             const bool first = __all_sync(0xffffffffu, total == 0 && g == 0);
@@ -392,7 +366,6 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
                 }
             }
         }
-#endif
         total += my_cnt + s_rej[tid];
         s_thr[tid] = r[15];                          // 16th smallest key so far (MAX if < 16)
         __syncthreads();
