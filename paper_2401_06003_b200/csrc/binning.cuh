@@ -162,30 +162,36 @@ __global__ void __launch_bounds__(kBinThreads) k_count(Params P, int8_t* __restr
 // --------------------------------------------------------------------------- k_tscan
 
 // One CTA: tile_off <- exclusive scan of the tile totals (tile_off[T] = M); tile_kbase <-
-// exclusive scan of the kept-list capacity min(16 * 256, 4 * pairs(t)).
+// exclusive scan of the kept-list capacity min(16 * 256, 4 * pairs(t)) (16 * 256 under coarse
+// inclusion: dense lists).
 __global__ void __launch_bounds__(1024) k_tscan(Params P)
 {
+    // each thread owns a contiguous run of tiles: local sums, one block-wide scan of the
+    // packed (pairs, capacity) sums, then the run's offsets (both totals < 2^32)
     __shared__ uint32_t s_ws[32];
+    __shared__ uint32_t s_ws2[32];
     const int T = P.T;
-    uint32_t ca = 0, cb = 0;
-    for (int base = 0; base < T; base += blockDim.x) {
-        const int t = base + threadIdx.x;
-        const uint32_t a = t < T ? P.tile_off[t] : 0u;
-        // coarse inclusion: dense 16 per pixel (a pixel's merged list can exceed its own)
-        const uint32_t b = P.coarse ? (uint32_t)(kTilePix * kCap) : min(4u * a, (uint32_t)(kTilePix * kCap));
-        uint32_t ta, tb;
-        const uint32_t pa = block_excl_scan(a, s_ws, &ta);
-        const uint32_t pb = block_excl_scan(t < T ? b : 0u, s_ws, &tb);
-        if (t < T) {
-            P.tile_off[t] = ca + pa;
-            P.tile_kbase[t] = cb + pb;
-        }
-        ca += ta;
-        cb += tb;
+    const int per = (T + blockDim.x - 1) / blockDim.x;
+    const int t0 = min(T, (int)threadIdx.x * per), t1 = min(T, t0 + per);
+    uint32_t sa = 0, sb = 0;
+    for (int t = t0; t < t1; ++t) {
+        const uint32_t a = P.tile_off[t];
+        sa += a;
+        sb += P.coarse ? (uint32_t)(kTilePix * kCap) : min(4u * a, (uint32_t)(kTilePix * kCap));
+    }
+    uint32_t ta, tb;
+    uint32_t pa = block_excl_scan(sa, s_ws, &ta);
+    uint32_t pb = block_excl_scan(sb, s_ws2, &tb);
+    for (int t = t0; t < t1; ++t) {
+        const uint32_t a = P.tile_off[t];
+        P.tile_off[t] = pa;
+        P.tile_kbase[t] = pb;
+        pa += a;
+        pb += P.coarse ? (uint32_t)(kTilePix * kCap) : min(4u * a, (uint32_t)(kTilePix * kCap));
     }
     if (threadIdx.x == 0) {
-        P.tile_off[T] = ca;
-        P.tile_kbase[T] = cb;
+        P.tile_off[T] = ta;
+        P.tile_kbase[T] = tb;
     }
 }
 
