@@ -61,8 +61,8 @@ struct Params {
     uint32_t* pix_cnt;     // [T*256]  list length per tile pixel
     uint32_t* pix_meta;    // [T*256]  (local kept offset << 5) | K
     uint64_t* kept;        // [kcap]   kept (z, i) keys, per pixel in blend order; with coarse
-                           //          inclusion (z, i << 4 | d), dense 16 per pixel
-    uint64_t* own;         // [T*256*16] coarse inclusion only: each pixel's own sorted top-16
+                           //          inclusion (z, i << 4 | d), dense [tile][m][pixel]
+    uint64_t* own;         // [T][16][256] coarse inclusion only: each pixel's own sorted top-16
     float* kept_gamma;     // [kcap]   gamma of each kept fragment (saved for the backward)
     unsigned long long* stats;  // [8]  n_culled, n_visible, n_pairs, n_frag, n_kept, n_trunc, max_list
 };

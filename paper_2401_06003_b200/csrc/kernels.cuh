@@ -375,10 +375,11 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
     if constexpr (COARSE) {
         P.pix_cnt[(size_t)t * kTilePix + tid] = valid ? total : 0u;
         const int Ko = valid ? (int)min(total, (uint32_t)kCap) : 0;
-        uint64_t* op = P.own + ((size_t)t * kTilePix + tid) * kCap;
+        // [tile][m][pixel] so that a warp's m-th keys are contiguous (coalesced both ways)
+        uint64_t* op = P.own + (size_t)t * kTilePix * kCap + tid;
 #pragma unroll
         for (int mm = 0; mm < kCap; ++mm)
-            if (mm < Ko) op[mm] = r[mm];
+            if (mm < Ko) op[(size_t)mm * kTilePix] = r[mm];
         return;
     }
 
@@ -484,23 +485,24 @@ __global__ void __launch_bounds__(kTilePix) k_coarse_blend(Params P, float* __re
     for (int d = 0; d <= D; ++d) {
         const LayerGeom& A = P.L[tc.l + d];
         const int ax = px >> d, ay = py >> d;
-        const size_t slot = (size_t)(A.tile_base + (ay >> 4) * A.tiles_x + (ax >> 4)) * kTilePix
-                          + (size_t)((ay & (kTile - 1)) * kTile + (ax & (kTile - 1)));
-        const int kd = valid ? (int)min(__ldg(P.pix_cnt + slot), (uint32_t)kCap) : 0;
+        const size_t at = (size_t)(A.tile_base + (ay >> 4) * A.tiles_x + (ax >> 4));
+        const int aq = (ay & (kTile - 1)) * kTile + (ax & (kTile - 1));
+        const int kd = valid ? (int)min(__ldg(P.pix_cnt + at * kTilePix + aq), (uint32_t)kCap) : 0;
         if (__all_sync(0xffffffffu, kd == 0)) continue;
         K += kd;
-        const uint64_t* op = P.own + slot * kCap;
+        const unsigned long long* op = reinterpret_cast<const unsigned long long*>(P.own) + at * kTilePix * kCap + aq;
         uint64_t tk[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-            const uint64_t k = j < kd ? __ldg(reinterpret_cast<const unsigned long long*>(op) + j) : kKeyMax;
+            const uint64_t k = j < kd ? __ldg(op + (size_t)j * kTilePix) : kKeyMax;
             tk[j] = j < kd ? ((k & 0xffffffff00000000ull) | ((k & 0xffffffffull) << 4) | (uint64_t)d) : kKeyMax;
         }
         merge_keep16<16>(r, tk);
     }
     K = min(K, kCap);
 
-    const size_t kidx = (size_t)P.tile_kbase[t] + (size_t)tid * kCap;
+    // dense kept lists, [tile][m][pixel] (stride kTilePix between a pixel's entries)
+    const size_t kidx = (size_t)P.tile_kbase[t] + (size_t)tid;
     float C[FC];
 #pragma unroll
     for (int c = 0; c < FC; ++c) C[c] = 0.f;
@@ -533,7 +535,7 @@ __global__ void __launch_bounds__(kTilePix) k_coarse_blend(Params P, float* __re
                 }
                 A += tg;
                 T = __fmul_rn(T, __fsub_rn(1.0f, w.gamma));
-                if (save) P.kept_gamma[kidx + mm] = w.gamma;
+                if (save) P.kept_gamma[kidx + (size_t)mm * kTilePix] = w.gamma;
                 if (T < P.t_min) Keff = mm + 1;
             }
         }
@@ -546,12 +548,12 @@ __global__ void __launch_bounds__(kTilePix) k_coarse_blend(Params P, float* __re
             if (c < P.F) out[c * plane] = C[c];
         out[P.F * plane] = A;
     }
-    P.pix_meta[(size_t)t * kTilePix + tid] = ((uint32_t)(tid * kCap) << 5) | (uint32_t)Keff;
+    P.pix_meta[(size_t)t * kTilePix + tid] = ((uint32_t)tid << 5) | (uint32_t)Keff;
     if (save) {
         uint64_t* kp = P.kept + kidx;
 #pragma unroll
         for (int mm = 0; mm < kCap; ++mm)
-            if (mm < Keff) kp[mm] = r[mm];
+            if (mm < Keff) kp[(size_t)mm * kTilePix] = r[mm];
     }
 }
 
@@ -621,6 +623,7 @@ __global__ void __launch_bounds__(kTilePix, FC <= 4 ? TRIPS_BWD_CTAS : 2) k_back
     const size_t kidx = (size_t)P.tile_kbase[t] + (meta >> 5);
     const uint64_t* kp = P.kept + kidx;
     const float* gm = P.kept_gamma + kidx;
+    constexpr int KS = COARSE ? kTilePix : 1;        // entry stride (coarse: [tile][m][pixel])
     float cg[CAM ? 17 : 1];
 #pragma unroll
     for (int k = 0; k < (CAM ? 17 : 1); ++k) cg[k] = 0.f;
@@ -644,7 +647,7 @@ __global__ void __launch_bounds__(kTilePix, FC <= 4 ? TRIPS_BWD_CTAS : 2) k_back
         for (int mm = 0; mm < kCap; ++mm) {
             if (mm < K) {
                 s_T[mm][tid] = T;
-                T = T * (1.0f - __ldg(gm + mm));
+                T = T * (1.0f - __ldg(gm + mm * KS));
             }
         }
     }
@@ -653,7 +656,7 @@ __global__ void __launch_bounds__(kTilePix, FC <= 4 ? TRIPS_BWD_CTAS : 2) k_back
     float T = 1.f;
 #pragma unroll
     for (int mm = 0; mm < kCap; ++mm) {
-        gam[mm] = mm < K ? __ldg(gm + mm) : 0.f;
+        gam[mm] = mm < K ? __ldg(gm + mm * KS) : 0.f;
         Tm[mm] = T;
         T = T * (1.0f - gam[mm]);
     }
@@ -674,7 +677,7 @@ __global__ void __launch_bounds__(kTilePix, FC <= 4 ? TRIPS_BWD_CTAS : 2) k_back
 #pragma unroll
         for (int u = 0; u < kBatch; ++u) {
             const int mm = min(b * kBatch + u, K - 1);
-            kb[u] = __ldg(reinterpret_cast<const unsigned long long*>(kp) + mm);
+            kb[u] = __ldg(reinterpret_cast<const unsigned long long*>(kp) + mm * KS);
             const uint32_t iu = COARSE ? (uint32_t)kb[u] >> 4 : (uint32_t)kb[u];
             gather_record<FC>(P, iu, rb[u]);
         }
@@ -689,7 +692,7 @@ __global__ void __launch_bounds__(kTilePix, FC <= 4 ? TRIPS_BWD_CTAS : 2) k_back
             const float4 r0 = rb[u][0];
             const FragW w = frag_weights(r0, tc.l + d, P.n_layers, px >> d, py >> d);
 #if TRIPS_BWD_SMEM_T
-            const float g = __ldg(gm + mm), tm = s_T[mm][tid];
+            const float g = __ldg(gm + mm * KS), tm = s_T[mm][tid];
 #else
             const float g = gam[mm], tm = Tm[mm];
 #endif
@@ -758,7 +761,7 @@ __global__ void __launch_bounds__(kTilePix) k_export(Params P, int what, void* d
         const uint64_t* kp = P.kept + P.tile_kbase[t] + (meta >> 5);
         int32_t* o = static_cast<int32_t*>(dst) + pidx * kCap;
         for (int m = 0; m < kCap; ++m) {
-            const uint32_t lo = (uint32_t)kp[m];
+            const uint32_t lo = (uint32_t)kp[P.coarse ? m * kTilePix : m];
             if (what == 3) o[m] = m < K ? (P.coarse ? (int32_t)(lo & 15u) : 0) : -1;
             else o[m] = m < K ? (int32_t)(P.coarse ? lo >> 4 : lo) : -1;
         }
