@@ -108,9 +108,6 @@ __global__ void __launch_bounds__(kBinThreads) k_count(Params P, int8_t* __restr
         const bool vis = project_exact(P.cam, in[u][0], in[u][1], in[u][2], in[u][3], xs, ys, z, s);
         float4* r = reinterpret_cast<float4*>(P.rec + (size_t)i * P.RS);
         r[0] = make_float4(vis ? xs : 0.f, vis ? ys : 0.f, vis ? s : kCulled, in[u][4]);
-#if TRIPS_SPLIT_REC
-        r = reinterpret_cast<float4*>(P.tau + (size_t)i * FC) - 1;     // r[1 + c] = tau block c
-#endif
         const float* d = P.desc + (size_t)i * P.F;
         if (vec_desc) {
 #pragma unroll
@@ -208,30 +205,15 @@ __global__ void __launch_bounds__(kBinThreads, kBinCtasPerSm) k_emit(Params P)
     __syncthreads();
     int b, e;
     cta_range(P.n, b, e);
-#ifndef TRIPS_EMIT_UNROLL
-#define TRIPS_EMIT_UNROLL 1
-#endif
-    constexpr int kU = TRIPS_EMIT_UNROLL;         // points per thread per iteration (loads issued together)
-    for (int i0 = b + threadIdx.x; i0 < e; i0 += kU * blockDim.x) {
-        float4 r0[kU];
-        float zz[kU];
-#pragma unroll
-        for (int u = 0; u < kU; ++u) {
-            const int i = min(i0 + u * (int)blockDim.x, e - 1);
-            r0[u] = __ldg(reinterpret_cast<const float4*>(P.rec + (size_t)i * P.RS));
-            zz[u] = __ldg(P.zbuf + i);
-        }
-#pragma unroll
-        for (int u = 0; u < kU; ++u) {
-            const int i = i0 + u * (int)blockDim.x;
-            if (i >= e || !(r0[u].z >= 0.f)) continue;            // past the range / culled
-            const uint64_t key = ((uint64_t)__float_as_uint(zz[u]) << 32) | (uint32_t)i;
-            for_each_pair(P, r0[u].x, r0[u].y, r0[u].z, [&](int t, uint32_t o) {
-                const uint32_t pos = atomicAdd(&s_cur[t], 1u);
-                P.bin_key[pos] = key;
-                P.bin_orig[pos] = (uint16_t)o;
-            });
-        }
+    for (int i = b + threadIdx.x; i < e; i += blockDim.x) {
+        const float4 r0 = __ldg(reinterpret_cast<const float4*>(P.rec + (size_t)i * P.RS));
+        if (!(r0.z >= 0.f)) continue;                             // culled
+        const uint64_t key = ((uint64_t)__float_as_uint(__ldg(P.zbuf + i)) << 32) | (uint32_t)i;
+        for_each_pair(P, r0.x, r0.y, r0.z, [&](int t, uint32_t o) {
+            const uint32_t pos = atomicAdd(&s_cur[t], 1u);
+            P.bin_key[pos] = key;
+            P.bin_orig[pos] = (uint16_t)o;
+        });
     }
 }
 

@@ -15,9 +15,7 @@ constexpr int kTile = 16;                 // pyramid tiles are 16 x 16 pixels
 constexpr int kTilePix = kTile * kTile;   // one CTA thread per tile pixel
 constexpr int kCap = 16;                  // "clamped to a maximum size of 16"
 constexpr int kMaxLayers = 16;
-#ifndef TRIPS_SPLIT_REC
-#define TRIPS_SPLIT_REC 0      // descriptors in their own array instead of inside the record
-#endif
+
 constexpr float kEps = 0.25f;             // "at least eps = 0.25"
 constexpr uint64_t kKeyMax = ~0ull;
 constexpr float kCulled = -1.0f;          // rec.s marker of a culled point
@@ -43,14 +41,12 @@ struct Params {
     int32_t n_layers, T;              // layers, total tiles
     float t_min;                      // T_min blend variant (0 = the exact definition)
     int32_t coarse;                   // coarse-layer inclusion depth (0 = the exact definition)
-    int32_t sched_D, sched_G, sched_S; // per-tile CTA schedule (kernels.cuh block_tile)
     LayerGeom L[kMaxLayers];
     Cam cam;
     // inputs (caller)
     const float* pos; const float* sw; const float* alpha; const float* desc;
     // workspace
-    float* rec;            // [n][RS]  (x, y, s, alpha[, tau[FC]])   s < 0 marks culled
-    float* tau;            // [n][FC]  descriptors (TRIPS_SPLIT_REC builds; else inside rec)
+    float* rec;            // [n][RS]  (x, y, s, alpha, tau[FC])     s < 0 marks culled
     float* zbuf;           // [n]      view depth z
     uint32_t* hist;        // [C][T]   per-CTA tile counts -> per-CTA offsets within the tile
     uint32_t* cta_vis;     // [C]      visible points per binning CTA (statistics)
@@ -258,16 +254,9 @@ __device__ __forceinline__ void cswap(uint64_t& a, uint64_t& b)
 template <int FC>
 __device__ __forceinline__ void gather_record(const Params& P, uint32_t i, float4 (&rb)[1 + FC / 4])
 {
-#if TRIPS_SPLIT_REC
-    rb[0] = __ldg(reinterpret_cast<const float4*>(P.rec) + i);
-    const float4* tp = reinterpret_cast<const float4*>(P.tau) + (size_t)i * (FC / 4);
-#pragma unroll
-    for (int c4 = 0; c4 < FC / 4; ++c4) rb[1 + c4] = __ldg(tp + c4);
-#else
     const float4* rp = reinterpret_cast<const float4*>(P.rec + (size_t)i * P.RS);
 #pragma unroll
     for (int c4 = 0; c4 <= FC / 4; ++c4) rb[c4] = __ldg(rp + c4);
-#endif
 }
 
 }  // namespace trips

@@ -24,17 +24,8 @@ namespace trips {
 #ifndef TRIPS_RASTER_CTAS
 #define TRIPS_RASTER_CTAS 3
 #endif
-#ifndef TRIPS_PRELOAD
-#define TRIPS_PRELOAD 1
-#endif
-#ifndef TRIPS_BWD_SMEM_T
-#define TRIPS_BWD_SMEM_T 0
-#endif
 #ifndef TRIPS_BWD_CTAS
 #define TRIPS_BWD_CTAS 3
-#endif
-#ifndef TRIPS_BLEND_PREFETCH
-#define TRIPS_BLEND_PREFETCH 0
 #endif
 constexpr int kChunk = TRIPS_CHUNK;         // (point, tile) pairs staged per K4 iteration
 constexpr int kPairsPerThread = kChunk / kTilePix;
@@ -167,48 +158,6 @@ __device__ __forceinline__ TileCoord tile_coord(const Params& P, int t)
     return c;
 }
 
-// Tile schedule of the per-tile kernels.  CTAs visit the pyramid group by group:
-// a group is one tile of layer D = sched_D with all its descendant tiles in layers D-1..0, in
-// quadtree post-order (the four children before their parent), so a point's two adjacent
-// layers are processed close in time and its record and gradient row are reused from L2
-// instead of being fetched again after a whole layer.  Layers above D follow in natural
-// order.  Slots whose tile lies outside the layer (ragged image borders) exit at once.
-#ifndef TRIPS_GROUP_DEPTH
-#define TRIPS_GROUP_DEPTH 0     // measured slower than the natural order (profiles/r01_v2.md)
-#endif
-__device__ __forceinline__ bool block_tile(const Params& P, int b, int& t, TileCoord& tc)
-{
-#if TRIPS_GROUP_DEPTH == 0
-    t = b;
-    tc = tile_coord(P, t);
-    return true;
-#endif
-    const int D = P.sched_D;
-    const int nb = P.sched_G * P.sched_S;
-    if (D == 0 || b >= nb) {
-        t = D == 0 ? b : P.L[D + 1].tile_base + (b - nb);
-        tc = tile_coord(P, t);
-        return true;
-    }
-    const int g = b / P.sched_S;
-    int k = b - g * P.sched_S;
-    int l = D;
-    int x = g % P.L[D].tiles_x, y = g / P.L[D].tiles_x;
-#pragma unroll 1
-    while (k != ((1 << (2 * (l + 1))) - 1) / 3 - 1) {    // subtree of layer l: (4^(l+1) - 1) / 3 tiles
-        const int sc = ((1 << (2 * l)) - 1) / 3;         // child subtree size
-        const int c = k / sc;
-        k -= c * sc;
-        --l;
-        x = 2 * x + (c & 1);
-        y = 2 * y + (c >> 1);
-    }
-    if (x >= P.L[l].tiles_x || y >= P.L[l].tiles_y) return false;
-    t = P.L[l].tile_base + y * P.L[l].tiles_x + x;
-    tc.l = l; tc.tx = x; tc.ty = y;
-    return true;
-}
-
 // --------------------------------------------------------------------------- K4 raster
 
 // Dynamic shared memory of k_raster: the per-chunk fragment keys.  (Reusing it after the last
@@ -234,9 +183,8 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
     __shared__ uint64_t s_thr[kTilePix];             // per-pixel 16th smallest key so far
     __shared__ uint32_t s_warp[32];
 
-    int t;
-    TileCoord tc;
-    if (!block_tile(P, blockIdx.x, t, tc)) return;
+    const int t = blockIdx.x;
+    const TileCoord tc = tile_coord(P, t);
     const LayerGeom& G = P.L[tc.l];
     const int tid = threadIdx.x;
     const int lx = tid & (kTile - 1), ly = tid >> 4;
@@ -269,7 +217,6 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
         // cloud hit the same pixels, and same-address shared atomics within a warp serialise.
         uint32_t fq[kPairsPerThread][4];             // (q | rank << 8), 0xffffffff = none
         const int jl = (tid & 31) * 8 + (tid >> 5);
-#if TRIPS_PRELOAD
         // all of this thread's pair loads issued before the first shared-memory atomic (a
         // generic-pointer load cannot be hoisted across them); keys stay live for phase B
         uint64_t pk[kPairsPerThread];
@@ -280,20 +227,14 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
             pk[k] = j < m ? __ldg(reinterpret_cast<const unsigned long long*>(P.bin_key) + c0 + (size_t)j * nch) : 0ull;
             po[k] = j < m ? __ldg(P.bin_orig + c0 + (size_t)j * nch) : 0u;
         }
-#endif
 #pragma unroll
         for (int k = 0; k < kPairsPerThread; ++k) {
 #pragma unroll
             for (int c = 0; c < 4; ++c) fq[k][c] = 0xffffffffu;
             const int j = jl + k * kTilePix;
             if (j < m) {
-#if TRIPS_PRELOAD
                 const uint64_t key = pk[k];
                 const uint32_t o = po[k];
-#else
-                const uint64_t key = P.bin_key[c0 + (size_t)j * nch];
-                const uint32_t o = P.bin_orig[c0 + (size_t)j * nch];
-#endif
                 const int q0 = (int)(o & 31u) - 1 + ((int)((o >> 5) & 31u) - 1) * kTile;   // may be < 0
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
@@ -325,11 +266,7 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
         for (int k = 0; k < kPairsPerThread; ++k) {
             const int j = jl + k * kTilePix;
             if (j < m) {
-#if TRIPS_PRELOAD
                 const uint64_t key = pk[k];
-#else
-                const uint64_t key = P.bin_key[c0 + (size_t)j * nch];
-#endif
 #pragma unroll
                 for (int c = 0; c < 4; ++c)
                     if (fq[k][c] != 0xffffffffu) s_keys[s_base[fq[k][c] & 0xffu] + (fq[k][c] >> 8)] = key;
@@ -398,12 +335,6 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
     // T_min variant (0 = the exact definition): the kept list ends with
     // the fragment after which the fp32 transmittance drops below t_min
     int Keff = K;
-#if TRIPS_BLEND_PREFETCH
-    // pull every kept record towards L1 before the dependent batch loop (no registers held)
-#pragma unroll
-    for (int mm = 0; mm < kCap; ++mm)
-        if (mm < K) asm volatile("prefetch.global.L1 [%0];" :: "l"(P.rec + (size_t)(uint32_t)r[mm] * P.RS));
-#endif
 #pragma unroll
     for (int b = 0; b < kCap / kBlendBatch; ++b) {
         if (b * kBlendBatch >= Keff || (!save && T == 0.f)) break;
@@ -469,9 +400,8 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
 template <int FC>
 __global__ void __launch_bounds__(kTilePix) k_coarse_blend(Params P, float* __restrict__ pyramid, int save)
 {
-    int t;
-    TileCoord tc;
-    if (!block_tile(P, blockIdx.x, t, tc)) return;
+    const int t = blockIdx.x;
+    const TileCoord tc = tile_coord(P, t);
     const LayerGeom& G = P.L[tc.l];
     const int tid = threadIdx.x;
     const int px = tc.tx * kTile + (tid & (kTile - 1)), py = tc.ty * kTile + (tid >> 4);
@@ -611,9 +541,8 @@ template <int FC, bool CAM, bool COARSE>
 __global__ void __launch_bounds__(kTilePix, FC <= 4 ? TRIPS_BWD_CTAS : 2) k_backward(Params P, const float* __restrict__ gpyr,
                                                        float* __restrict__ grad, float* __restrict__ grad_cam)
 {
-    int t;
-    TileCoord tc;
-    if (!block_tile(P, blockIdx.x, t, tc)) return;
+    const int t = blockIdx.x;
+    const TileCoord tc = tile_coord(P, t);
     const LayerGeom& G = P.L[tc.l];
     const int tid = threadIdx.x;
     const int px = tc.tx * kTile + (tid & (kTile - 1)), py = tc.ty * kTile + (tid >> 4);
@@ -637,21 +566,6 @@ __global__ void __launch_bounds__(kTilePix, FC <= 4 ? TRIPS_BWD_CTAS : 2) k_back
     const float gA = K > 0 ? __ldg(gp + P.F * plane) : 0.f;
 
     // T_m from the saved gamma_m (Eq. 6) -- no record gathers
-#if TRIPS_BWD_SMEM_T
-    // T_m staged in shared memory ([m][pixel], conflict-free) and gamma_m re-read from L1 in
-    // the reverse loop: 32 fewer live registers
-    __shared__ float s_T[kCap][kTilePix];
-    {
-        float T = 1.f;
-#pragma unroll
-        for (int mm = 0; mm < kCap; ++mm) {
-            if (mm < K) {
-                s_T[mm][tid] = T;
-                T = T * (1.0f - __ldg(gm + mm * KS));
-            }
-        }
-    }
-#else
     float gam[kCap], Tm[kCap];
     float T = 1.f;
 #pragma unroll
@@ -660,7 +574,6 @@ __global__ void __launch_bounds__(kTilePix, FC <= 4 ? TRIPS_BWD_CTAS : 2) k_back
         Tm[mm] = T;
         T = T * (1.0f - gam[mm]);
     }
-#endif
     // reverse replay with suffix recurrences (division-free):
     //   dL/dgamma_m = T_m (<gC, tau_m - B_m> + gA (1 - b_m)),
     //   B_{m-1} = gamma_m tau_m + (1 - gamma_m) B_m,   b_{m-1} = gamma_m + (1 - gamma_m) b_m
@@ -691,11 +604,7 @@ __global__ void __launch_bounds__(kTilePix, FC <= 4 ? TRIPS_BWD_CTAS : 2) k_back
             const float z = __uint_as_float((uint32_t)(kb[u] >> 32));
             const float4 r0 = rb[u][0];
             const FragW w = frag_weights(r0, tc.l + d, P.n_layers, px >> d, py >> d);
-#if TRIPS_BWD_SMEM_T
-            const float g = __ldg(gm + mm * KS), tm = s_T[mm][tid];
-#else
             const float g = gam[mm], tm = Tm[mm];
-#endif
             float tau[FC];
 #pragma unroll
             for (int c4 = 0; c4 < FC / 4; ++c4) {

@@ -35,14 +35,13 @@ struct trips_plan {
     int32_t n_layers, F, FC, RS, G, W, H, T;
     float t_min;
     int32_t coarse;         // coarse-layer inclusion depth, clamped to n_layers - 1
-    int32_t sched_D, sched_G, sched_S, tile_grid;   // per-tile CTA schedule (block_tile)
     int64_t max_points, P, pyr_floats;
     LayerGeom L[kMaxLayers];
     uint64_t kcap;
     // workspace layout (byte offsets)
     int32_t ctas;           // binning CTAs (persistent grid)
     size_t off_rec, off_z, off_hist, off_cvis, off_toff, off_tkb, off_bkey, off_borig, off_pcnt, off_pmeta, off_kept, off_kgam,
-        off_own, off_tau, off_stats, ws_bytes;
+        off_own, off_stats, ws_bytes;
     // state
     const void* ws_bound = nullptr;
     int stage = 0;          // 0 none, 1 projected, 2 forward (saved), 3 forward (not saved)
@@ -148,13 +147,11 @@ Params make_params(const trips_plan* p, void* ws)
     P.n_layers = p->n_layers; P.T = p->T;
     P.t_min = p->t_min;
     P.coarse = p->coarse;
-    P.sched_D = p->sched_D; P.sched_G = p->sched_G; P.sched_S = p->sched_S;
     for (int l = 0; l < kMaxLayers; ++l) P.L[l] = p->L[l];
     P.cam = p->cam;
     char* b = static_cast<char*>(ws);
     P.rec = reinterpret_cast<float*>(b + p->off_rec);
     P.zbuf = reinterpret_cast<float*>(b + p->off_z);
-    P.tau = reinterpret_cast<float*>(b + p->off_tau);
     P.hist = reinterpret_cast<uint32_t*>(b + p->off_hist);
     P.cta_vis = reinterpret_cast<uint32_t*>(b + p->off_cvis);
     P.tile_off = reinterpret_cast<uint32_t*>(b + p->off_toff);
@@ -201,7 +198,7 @@ int trips_plan_create(const trips_config* cfg, int32_t width, int32_t height, in
     if (width < 1 || height < 1 || width > 32768 || height > 32768) return TRIPS_ERR_ARG;
     if (max_points < 0 || max_points >= (int64_t(1) << 28)) return TRIPS_ERR_ARG;
     trips_plan* p = new trips_plan();
-    p->n_layers = n; p->F = F; p->FC = (F + 3) & ~3; p->RS = TRIPS_SPLIT_REC ? 4 : 4 + p->FC; p->G = 8 + p->FC;
+    p->n_layers = n; p->F = F; p->FC = (F + 3) & ~3; p->RS = 4 + p->FC; p->G = 8 + p->FC;
     p->t_min = cfg->t_min;
     p->coarse = std::min(cfg->coarse_layers, n - 1);
     p->W = width; p->H = height; p->max_points = max_points;
@@ -222,18 +219,6 @@ int trips_plan_create(const trips_config* cfg, int32_t width, int32_t height, in
     }
     p->P = pix;
     p->T = tiles;
-    // grouped tile schedule: one layer-D tile + its descendants per group (kernels.cuh)
-    p->sched_D = std::min(TRIPS_GROUP_DEPTH, n - 1);
-    if (p->sched_D > 0) {
-        const int D = p->sched_D;
-        p->sched_G = p->L[D].tiles_x * p->L[D].tiles_y;
-        p->sched_S = ((1 << (2 * (D + 1))) - 1) / 3;
-        const int rest = D + 1 < n ? tiles - p->L[D + 1].tile_base : 0;
-        p->tile_grid = p->sched_G * p->sched_S + rest;
-    } else {
-        p->sched_G = p->sched_S = 0;
-        p->tile_grid = tiles;
-    }
     p->pyr_floats = pix * (F + 1);
     const uint64_t kc1 = (uint64_t)tiles * kTilePix * kCap, kc2 = (uint64_t)max_points * 32;
     p->kcap = (p->coarse || kc1 < kc2) ? kc1 : kc2;    // coarse inclusion: dense 16 per pixel
@@ -243,7 +228,6 @@ int trips_plan_create(const trips_config* cfg, int32_t width, int32_t height, in
     p->ctas = num_sms() * kBinCtasPerSm;
     p->off_rec = o;    o = align256(o + N * p->RS * sizeof(float));
     p->off_z = o;      o = align256(o + N * sizeof(float));
-    p->off_tau = o;    o = align256(o + (TRIPS_SPLIT_REC ? N * p->FC * sizeof(float) : 0));
     p->off_hist = o;   o = align256(o + (size_t)p->ctas * tiles * 4);
     p->off_cvis = o;   o = align256(o + (size_t)p->ctas * 4);
     p->off_toff = o;   o = align256(o + ((size_t)tiles + 1) * 4);
@@ -357,13 +341,13 @@ int trips_splat_forward(trips_plan* p, void* ws, float* pyramid, uint32_t flags,
             rattr[mode][p->FC / 4] = true;
         }
         if (mode == kRasterOwn) {
-            TRIPS_FC_SWITCH(p->FC, (k_raster<kFC, kRasterOwn><<<p->tile_grid, kTilePix, rsm, st>>>(P, pyramid, save)));
+            TRIPS_FC_SWITCH(p->FC, (k_raster<kFC, kRasterOwn><<<p->T, kTilePix, rsm, st>>>(P, pyramid, save)));
             if ((rc = check_launch())) return rc;
-            TRIPS_FC_SWITCH(p->FC, (k_coarse_blend<kFC><<<p->tile_grid, kTilePix, 0, st>>>(P, pyramid, save)));
+            TRIPS_FC_SWITCH(p->FC, (k_coarse_blend<kFC><<<p->T, kTilePix, 0, st>>>(P, pyramid, save)));
         } else if (mode == kRasterTmin) {
-            TRIPS_FC_SWITCH(p->FC, (k_raster<kFC, kRasterTmin><<<p->tile_grid, kTilePix, rsm, st>>>(P, pyramid, save)));
+            TRIPS_FC_SWITCH(p->FC, (k_raster<kFC, kRasterTmin><<<p->T, kTilePix, rsm, st>>>(P, pyramid, save)));
         } else {
-            TRIPS_FC_SWITCH(p->FC, (k_raster<kFC, kRasterPlain><<<p->tile_grid, kTilePix, rsm, st>>>(P, pyramid, save)));
+            TRIPS_FC_SWITCH(p->FC, (k_raster<kFC, kRasterPlain><<<p->T, kTilePix, rsm, st>>>(P, pyramid, save)));
         }
         if ((rc = check_launch())) return rc;
     }
@@ -383,16 +367,16 @@ int trips_splat_backward(trips_plan* p, void* ws, const float* grad_pyramid, flo
     {
         StageScope sc(p, 4, st);
         if (grad_camera && p->coarse) {
-            TRIPS_FC_SWITCH(p->FC, (k_backward<kFC, true, true><<<p->tile_grid, kTilePix, 0, st>>>(P, grad_pyramid, grad,
+            TRIPS_FC_SWITCH(p->FC, (k_backward<kFC, true, true><<<p->T, kTilePix, 0, st>>>(P, grad_pyramid, grad,
                                                                                              grad_camera)));
         } else if (grad_camera) {
-            TRIPS_FC_SWITCH(p->FC, (k_backward<kFC, true, false><<<p->tile_grid, kTilePix, 0, st>>>(P, grad_pyramid, grad,
+            TRIPS_FC_SWITCH(p->FC, (k_backward<kFC, true, false><<<p->T, kTilePix, 0, st>>>(P, grad_pyramid, grad,
                                                                                               grad_camera)));
         } else if (p->coarse) {
-            TRIPS_FC_SWITCH(p->FC, (k_backward<kFC, false, true><<<p->tile_grid, kTilePix, 0, st>>>(P, grad_pyramid, grad,
+            TRIPS_FC_SWITCH(p->FC, (k_backward<kFC, false, true><<<p->T, kTilePix, 0, st>>>(P, grad_pyramid, grad,
                                                                                               nullptr)));
         } else {
-            TRIPS_FC_SWITCH(p->FC, (k_backward<kFC, false, false><<<p->tile_grid, kTilePix, 0, st>>>(P, grad_pyramid, grad,
+            TRIPS_FC_SWITCH(p->FC, (k_backward<kFC, false, false><<<p->T, kTilePix, 0, st>>>(P, grad_pyramid, grad,
                                                                                                nullptr)));
         }
         if ((rc = check_launch())) return rc;
