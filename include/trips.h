@@ -144,7 +144,11 @@ int32_t trips_grad_stride(const trips_plan* plan);
  *   pos        float[n][3] world positions, 4-byte aligned
  *   world_size float[n]    s_w
  *   opacity    float[n]    alpha
- *   desc       float[n][F] descriptors tau, row-major, 4-byte aligned
+ *   desc       float[n][F] descriptors tau, row-major, 4-byte aligned.  When F % 4 == 0 and
+ *              desc is 16-B aligned, trips_splat_forward/backward of this frame gather the
+ *              descriptors from these rows directly (no per-view copy): the caller keeps
+ *              desc allocated and unmodified until the frame's last forward/backward.
+ *              Otherwise a padded copy is taken here.
  *   level_out  int8[n]  nullable: -1 culled, else bits 0-3 lowest layer, 0x10 two layers,
  *                       0x20 eps branch (s < 1), 0x40 clamped (s >= 2^(n-1))
  *   proj_out   float[n][4] nullable: (x, y, z, s), NaN rows for culled points

@@ -85,20 +85,14 @@ __global__ void __launch_bounds__(kBinThreads) k_count(Params P, int8_t* __restr
 #define TRIPS_COUNT_UNROLL 1
 #endif
     constexpr int kU = TRIPS_COUNT_UNROLL;        // points per thread per iteration (loads issued together)
-    const bool vec_desc = P.F == FC && (reinterpret_cast<uintptr_t>(P.desc) & 15) == 0;
     for (int i0 = b + threadIdx.x; i0 < e; i0 += kU * blockDim.x) {
-      float in[kU][6];
-      float4 dv[kU][FC / 4];
+      float in[kU][5];
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
         const int i = min(i0 + u * (int)blockDim.x, e - 1);
         const float* q = P.pos + 3 * (size_t)i;
         in[u][0] = __ldg(q); in[u][1] = __ldg(q + 1); in[u][2] = __ldg(q + 2);
         in[u][3] = __ldg(P.sw + i); in[u][4] = __ldg(P.alpha + i);
-        if (vec_desc) {
-#pragma unroll
-            for (int c = 0; c < FC / 4; ++c) dv[u][c] = __ldg(reinterpret_cast<const float4*>(P.desc + (size_t)i * P.F) + c);
-        }
       }
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
@@ -106,19 +100,17 @@ __global__ void __launch_bounds__(kBinThreads) k_count(Params P, int8_t* __restr
         if (i >= e) break;
         float xs = 0.f, ys = 0.f, z = 0.f, s = 0.f;
         const bool vis = project_exact(P.cam, in[u][0], in[u][1], in[u][2], in[u][3], xs, ys, z, s);
-        float4* r = reinterpret_cast<float4*>(P.rec + (size_t)i * P.RS);
-        r[0] = make_float4(vis ? xs : 0.f, vis ? ys : 0.f, vis ? s : kCulled, in[u][4]);
-        const float* d = P.desc + (size_t)i * P.F;
-        if (vec_desc) {
-#pragma unroll
-            for (int c = 0; c < FC / 4; ++c) r[1 + c] = dv[u][c];
-        } else {
+        P.geo[i] = make_float4(vis ? xs : 0.f, vis ? ys : 0.f, vis ? s : kCulled, in[u][4]);
+        if (!P.tau_direct) {
+            // descriptors not gatherable in place (F % 4 != 0 or unaligned): padded copy
+            const float* d = P.desc + (size_t)i * P.F;
+            float4* r = reinterpret_cast<float4*>(P.tau_copy + (size_t)i * FC);
 #pragma unroll
             for (int c = 0; c < FC / 4; ++c) {
                 float v[4];
 #pragma unroll
                 for (int j = 0; j < 4; ++j) v[j] = (4 * c + j < P.F) ? __ldg(d + 4 * c + j) : 0.f;
-                r[1 + c] = make_float4(v[0], v[1], v[2], v[3]);
+                r[c] = make_float4(v[0], v[1], v[2], v[3]);
             }
         }
         P.zbuf[i] = z;
@@ -206,7 +198,7 @@ __global__ void __launch_bounds__(kBinThreads, kBinCtasPerSm) k_emit(Params P)
     int b, e;
     cta_range(P.n, b, e);
     for (int i = b + threadIdx.x; i < e; i += blockDim.x) {
-        const float4 r0 = __ldg(reinterpret_cast<const float4*>(P.rec + (size_t)i * P.RS));
+        const float4 r0 = __ldg(P.geo + i);
         if (!(r0.z >= 0.f)) continue;                             // culled
         const uint64_t key = ((uint64_t)__float_as_uint(__ldg(P.zbuf + i)) << 32) | (uint32_t)i;
         for_each_pair(P, r0.x, r0.y, r0.z, [&](int t, uint32_t o) {

@@ -37,7 +37,7 @@ struct Cam {
 
 // Everything a kernel needs, passed by value (fits the 32 KB kernel-parameter space).
 struct Params {
-    int32_t n, F, FC, RS, G;          // F features, FC = round_up(F,4), RS = 4 + FC, G = 8 + FC
+    int32_t n, F, FC, G;              // F features, FC = round_up(F,4), G = 8 + FC
     int32_t n_layers, T;              // layers, total tiles
     float t_min;                      // T_min blend variant (0 = the exact definition)
     int32_t coarse;                   // coarse-layer inclusion depth (0 = the exact definition)
@@ -46,8 +46,13 @@ struct Params {
     // inputs (caller)
     const float* pos; const float* sw; const float* alpha; const float* desc;
     // workspace
-    float* rec;            // [n][RS]  (x, y, s, alpha, tau[FC])     s < 0 marks culled
+    float4* geo;           // [n]      screen record (x, y, s, alpha); s < 0 marks culled
     float* zbuf;           // [n]      view depth z
+    float* tau_copy;       // [n][FC]  padded copy of desc, written only when !tau_direct
+    const float* tau;      // [n][FC]  descriptors gathered by raster/backward: the caller's desc
+                           //          itself when F % 4 == 0 and it is 16-B aligned (no per-view
+                           //          copy), else tau_copy
+    int32_t tau_direct;
     uint32_t* hist;        // [C][T]   per-CTA tile counts -> per-CTA offsets within the tile
     uint32_t* cta_vis;     // [C]      visible points per binning CTA (statistics)
     uint32_t* tile_off;    // [T+1]    first pair of each tile's bin; [T] = number of pairs M
@@ -249,14 +254,15 @@ __device__ __forceinline__ void cswap(uint64_t& a, uint64_t& b)
     a = lo; b = hi;
 }
 
-// Screen record of point i for the blend / backward gathers: rb[0] = (x, y, s, alpha),
-// rb[1 + c] = tau[4c .. 4c+3].
+// Screen record of point i for the blend / backward gathers: rb[0] = (x, y, s, alpha) from the
+// per-view record, rb[1 + c] = tau[4c .. 4c+3] from the (view-independent) descriptor rows.
 template <int FC>
 __device__ __forceinline__ void gather_record(const Params& P, uint32_t i, float4 (&rb)[1 + FC / 4])
 {
-    const float4* rp = reinterpret_cast<const float4*>(P.rec + (size_t)i * P.RS);
+    rb[0] = __ldg(P.geo + i);
+    const float4* tp = reinterpret_cast<const float4*>(P.tau + (size_t)i * FC);
 #pragma unroll
-    for (int c4 = 0; c4 <= FC / 4; ++c4) rb[c4] = __ldg(rp + c4);
+    for (int c4 = 0; c4 < FC / 4; ++c4) rb[1 + c4] = __ldg(tp + c4);
 }
 
 }  // namespace trips

@@ -32,7 +32,7 @@ struct EventPair {
 }  // namespace
 
 struct trips_plan {
-    int32_t n_layers, F, FC, RS, G, W, H, T;
+    int32_t n_layers, F, FC, G, W, H, T;
     float t_min;
     int32_t coarse;         // coarse-layer inclusion depth, clamped to n_layers - 1
     int64_t max_points, P, pyr_floats;
@@ -40,13 +40,15 @@ struct trips_plan {
     uint64_t kcap;
     // workspace layout (byte offsets)
     int32_t ctas;           // binning CTAs (persistent grid)
-    size_t off_rec, off_z, off_hist, off_cvis, off_toff, off_tkb, off_bkey, off_borig, off_pcnt, off_pmeta, off_kept, off_kgam,
+    size_t off_geo, off_tau, off_z, off_hist, off_cvis, off_toff, off_tkb, off_bkey, off_borig, off_pcnt, off_pmeta, off_kept, off_kgam,
         off_own, off_stats, ws_bytes;
     // state
     const void* ws_bound = nullptr;
     int stage = 0;          // 0 none, 1 projected, 2 forward (saved), 3 forward (not saved)
     int64_t n = 0;
     Cam cam;
+    const float* desc = nullptr;   // caller's descriptors of the last trips_project
+    bool tau_direct = false;       // gathered in place (F % 4 == 0, 16-B aligned)
     // profiling
     bool prof = false;
     std::vector<EventPair> pending[kStages];
@@ -143,14 +145,17 @@ Params make_params(const trips_plan* p, void* ws)
     Params P;
     memset(&P, 0, sizeof(P));
     P.n = (int32_t)p->n;
-    P.F = p->F; P.FC = p->FC; P.RS = p->RS; P.G = p->G;
+    P.F = p->F; P.FC = p->FC; P.G = p->G;
     P.n_layers = p->n_layers; P.T = p->T;
     P.t_min = p->t_min;
     P.coarse = p->coarse;
     for (int l = 0; l < kMaxLayers; ++l) P.L[l] = p->L[l];
     P.cam = p->cam;
     char* b = static_cast<char*>(ws);
-    P.rec = reinterpret_cast<float*>(b + p->off_rec);
+    P.geo = reinterpret_cast<float4*>(b + p->off_geo);
+    P.tau_copy = reinterpret_cast<float*>(b + p->off_tau);
+    P.tau_direct = p->tau_direct ? 1 : 0;
+    P.tau = p->tau_direct ? p->desc : P.tau_copy;
     P.zbuf = reinterpret_cast<float*>(b + p->off_z);
     P.hist = reinterpret_cast<uint32_t*>(b + p->off_hist);
     P.cta_vis = reinterpret_cast<uint32_t*>(b + p->off_cvis);
@@ -198,7 +203,7 @@ int trips_plan_create(const trips_config* cfg, int32_t width, int32_t height, in
     if (width < 1 || height < 1 || width > 32768 || height > 32768) return TRIPS_ERR_ARG;
     if (max_points < 0 || max_points >= (int64_t(1) << 28)) return TRIPS_ERR_ARG;
     trips_plan* p = new trips_plan();
-    p->n_layers = n; p->F = F; p->FC = (F + 3) & ~3; p->RS = 4 + p->FC; p->G = 8 + p->FC;
+    p->n_layers = n; p->F = F; p->FC = (F + 3) & ~3; p->G = 8 + p->FC;
     p->t_min = cfg->t_min;
     p->coarse = std::min(cfg->coarse_layers, n - 1);
     p->W = width; p->H = height; p->max_points = max_points;
@@ -226,7 +231,8 @@ int trips_plan_create(const trips_config* cfg, int32_t width, int32_t height, in
     const size_t N = (size_t)(max_points > 0 ? max_points : 1);
     size_t o = 0;
     p->ctas = num_sms() * kBinCtasPerSm;
-    p->off_rec = o;    o = align256(o + N * p->RS * sizeof(float));
+    p->off_geo = o;    o = align256(o + N * 16);
+    p->off_tau = o;    o = align256(o + N * p->FC * sizeof(float));   // used only when desc is not gatherable in place
     p->off_z = o;      o = align256(o + N * sizeof(float));
     p->off_hist = o;   o = align256(o + (size_t)p->ctas * tiles * 4);
     p->off_cvis = o;   o = align256(o + (size_t)p->ctas * 4);
@@ -286,6 +292,10 @@ int trips_project(trips_plan* p, void* ws, const trips_camera* c, int64_t n, con
     p->ws_bound = ws;
     p->stage = 0;
     p->n = n;
+    // descriptors are gathered straight from the caller's rows when they are whole float4s;
+    // otherwise k_count writes a padded copy into the workspace
+    p->desc = desc;
+    p->tau_direct = (p->F & 3) == 0 && aligned(desc, 16);
     Cam& cam = p->cam;
     cam.fx = c->fx; cam.fy = c->fy; cam.cx = c->cx; cam.cy = c->cy; cam.f = c->f;
     memcpy(cam.R, c->R, sizeof(cam.R));
