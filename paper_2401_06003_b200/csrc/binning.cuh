@@ -151,8 +151,8 @@ __global__ void __launch_bounds__(kBinThreads) k_count(Params P, int8_t* __restr
 // --------------------------------------------------------------------------- k_tscan
 
 // One CTA: tile_off <- exclusive scan of the tile totals (tile_off[T] = M); tile_kbase <-
-// exclusive scan of the kept-list capacity min(16 * 256, 4 * pairs(t)) (16 * 256 under coarse
-// inclusion: dense lists).
+// exclusive scan of the kept-list capacity: 16 * 256 per tile (dense [tile][m][pixel] lists, the
+// default), or min(16 * 256, 4 * pairs(t)) for compact per-pixel runs (TRIPS_DENSE_KEPT=0).
 __global__ void __launch_bounds__(1024) k_tscan(Params P)
 {
     // each thread owns a contiguous run of tiles: local sums, one block-wide scan of the
@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(1024) k_tscan(Params P)
     for (int t = t0; t < t1; ++t) {
         const uint32_t a = P.tile_off[t];
         sa += a;
-        sb += P.coarse ? (uint32_t)(kTilePix * kCap) : min(4u * a, (uint32_t)(kTilePix * kCap));
+        sb += (kDenseKept || P.coarse) ? (uint32_t)(kTilePix * kCap) : min(4u * a, (uint32_t)(kTilePix * kCap));
     }
     uint32_t ta, tb;
     uint32_t pa = block_excl_scan(sa, s_ws, &ta);
@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(1024) k_tscan(Params P)
         P.tile_off[t] = pa;
         P.tile_kbase[t] = pb;
         pa += a;
-        pb += P.coarse ? (uint32_t)(kTilePix * kCap) : min(4u * a, (uint32_t)(kTilePix * kCap));
+        pb += (kDenseKept || P.coarse) ? (uint32_t)(kTilePix * kCap) : min(4u * a, (uint32_t)(kTilePix * kCap));
     }
     if (threadIdx.x == 0) {
         P.tile_off[T] = ta;

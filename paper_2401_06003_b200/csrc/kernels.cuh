@@ -324,8 +324,12 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
     // Record gathers are issued kBatch at a time.  Without a following backward the loop
     // stops once T == 0 exactly (later terms vanish); with one, every gamma_m is needed.
     const int K = valid ? (int)min(total, (uint32_t)kCap) : 0;
-    uint32_t ktot;
-    const uint32_t koff = block_excl_scan((uint32_t)K, s_warp, &ktot);
+    uint32_t koff = (uint32_t)tid;                   // dense [tile][m][pixel]: entry m at kidx + m * KS
+    if constexpr (!kDenseKept) {
+        uint32_t ktot;
+        koff = block_excl_scan((uint32_t)K, s_warp, &ktot);
+    }
+    constexpr int KS = kDenseKept ? kTilePix : 1;
     TRIPS_PCLK(4);
     const size_t kidx = (size_t)P.tile_kbase[t] + koff;
     float C[FC];
@@ -361,7 +365,7 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
                 }
                 A += tg;
                 T = __fmul_rn(T, __fsub_rn(1.0f, w.gamma));      // pinned: decides the T_min cut
-                if (save) P.kept_gamma[kidx + mm] = w.gamma;
+                if (save) P.kept_gamma[kidx + (size_t)mm * KS] = w.gamma;
                 if (TMIN && T < P.t_min) Keff = mm + 1;
             }
         }
@@ -383,7 +387,7 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
         uint64_t* kp = P.kept + kidx;
 #pragma unroll
         for (int mm = 0; mm < kCap; ++mm)
-            if (mm < Keff) kp[mm] = r[mm];
+            if (mm < Keff) kp[(size_t)mm * KS] = r[mm];
     }
     TRIPS_PCLK(6);
 }
@@ -552,7 +556,7 @@ __global__ void __launch_bounds__(kTilePix, FC <= 4 ? TRIPS_BWD_CTAS : 2) k_back
     const size_t kidx = (size_t)P.tile_kbase[t] + (meta >> 5);
     const uint64_t* kp = P.kept + kidx;
     const float* gm = P.kept_gamma + kidx;
-    constexpr int KS = COARSE ? kTilePix : 1;        // entry stride (coarse: [tile][m][pixel])
+    constexpr int KS = (COARSE || kDenseKept) ? kTilePix : 1;   // entry stride (dense: [tile][m][pixel])
     float cg[CAM ? 17 : 1];
 #pragma unroll
     for (int k = 0; k < (CAM ? 17 : 1); ++k) cg[k] = 0.f;
@@ -670,7 +674,7 @@ __global__ void __launch_bounds__(kTilePix) k_export(Params P, int what, void* d
         const uint64_t* kp = P.kept + P.tile_kbase[t] + (meta >> 5);
         int32_t* o = static_cast<int32_t*>(dst) + pidx * kCap;
         for (int m = 0; m < kCap; ++m) {
-            const uint32_t lo = (uint32_t)kp[P.coarse ? m * kTilePix : m];
+            const uint32_t lo = (uint32_t)kp[(kDenseKept || P.coarse) ? m * kTilePix : m];
             if (what == 3) o[m] = m < K ? (P.coarse ? (int32_t)(lo & 15u) : 0) : -1;
             else o[m] = m < K ? (int32_t)(P.coarse ? lo >> 4 : lo) : -1;
         }

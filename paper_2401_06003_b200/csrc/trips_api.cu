@@ -226,7 +226,7 @@ int trips_plan_create(const trips_config* cfg, int32_t width, int32_t height, in
     p->T = tiles;
     p->pyr_floats = pix * (F + 1);
     const uint64_t kc1 = (uint64_t)tiles * kTilePix * kCap, kc2 = (uint64_t)max_points * 32;
-    p->kcap = (p->coarse || kc1 < kc2) ? kc1 : kc2;    // coarse inclusion: dense 16 per pixel
+    p->kcap = (kDenseKept || p->coarse || kc1 < kc2) ? kc1 : kc2;    // dense: 16 slots per pixel
     if (p->kcap >= (uint64_t(1) << 32) || tiles > kMaxTilesSmem) { delete p; return TRIPS_ERR_ARG; }
     const size_t N = (size_t)(max_points > 0 ? max_points : 1);
     size_t o = 0;

@@ -59,12 +59,14 @@ def test_plan_geometry(A):
     try:
         assert A.trips_num_pixels(plan) == 2_764_845           # P at 1080p, n=8
         small = A.trips_workspace_bytes(plan)
+        # kept lists are dense per tile, 16 slots per pixel: (8-B key + 4-B gamma) each
+        assert small >= 2_764_845 * 16 * (8 + 4)
     finally:
         A.trips_plan_destroy(plan)
-    # coarse-layer inclusion: + dense kept lists and own lists, 16 per tile pixel
+    # coarse-layer inclusion: + own lists, 16 per tile pixel
     plan = A.trips_plan_create(8, 4, 1920, 1080, 10, 0.0, 20)
     try:
-        assert A.trips_workspace_bytes(plan) >= small + 2_764_845 * 16 * (8 + 8 + 4)
+        assert A.trips_workspace_bytes(plan) >= small + 2_764_845 * 16 * 8
     finally:
         A.trips_plan_destroy(plan)
 
