@@ -150,38 +150,32 @@ __global__ void __launch_bounds__(kBinThreads) k_count(Params P, int8_t* __restr
 
 // --------------------------------------------------------------------------- k_tscan
 
-// One CTA: tile_off <- exclusive scan of the tile totals (tile_off[T] = M); tile_kbase <-
-// exclusive scan of the kept-list capacity: 16 * 256 per tile (dense [tile][m][pixel] lists, the
-// default), or min(16 * 256, 4 * pairs(t)) for compact per-pixel runs (TRIPS_DENSE_KEPT=0).
+// One CTA: tile_off <- exclusive scan of the tile totals (tile_off[T] = M).  The totals are
+// staged in shared memory with coalesced loads (T independent loads in flight instead of each
+// thread walking its run with dependent ones), each thread sums a contiguous run, one block scan.
 __global__ void __launch_bounds__(1024) k_tscan(Params P)
 {
-    // each thread owns a contiguous run of tiles: local sums, one block-wide scan of the
-    // packed (pairs, capacity) sums, then the run's offsets (both totals < 2^32)
+    extern __shared__ __align__(16) uint32_t s_tot[];             // [T]
     __shared__ uint32_t s_ws[32];
-    __shared__ uint32_t s_ws2[32];
     const int T = P.T;
+#pragma unroll 4
+    for (int t = threadIdx.x; t < T; t += blockDim.x) s_tot[t] = P.tile_off[t];
+    __syncthreads();
     const int per = (T + blockDim.x - 1) / blockDim.x;
     const int t0 = min(T, (int)threadIdx.x * per), t1 = min(T, t0 + per);
-    uint32_t sa = 0, sb = 0;
-    for (int t = t0; t < t1; ++t) {
-        const uint32_t a = P.tile_off[t];
-        sa += a;
-        sb += (kDenseKept || P.coarse) ? (uint32_t)(kTilePix * kCap) : min(4u * a, (uint32_t)(kTilePix * kCap));
-    }
-    uint32_t ta, tb;
+    uint32_t sa = 0;
+    for (int t = t0; t < t1; ++t) sa += s_tot[t];
+    uint32_t ta;
     uint32_t pa = block_excl_scan(sa, s_ws, &ta);
-    uint32_t pb = block_excl_scan(sb, s_ws2, &tb);
     for (int t = t0; t < t1; ++t) {
-        const uint32_t a = P.tile_off[t];
-        P.tile_off[t] = pa;
-        P.tile_kbase[t] = pb;
+        const uint32_t a = s_tot[t];
+        s_tot[t] = pa;
         pa += a;
-        pb += (kDenseKept || P.coarse) ? (uint32_t)(kTilePix * kCap) : min(4u * a, (uint32_t)(kTilePix * kCap));
     }
-    if (threadIdx.x == 0) {
-        P.tile_off[T] = ta;
-        P.tile_kbase[T] = tb;
-    }
+    __syncthreads();
+#pragma unroll 4
+    for (int t = threadIdx.x; t < T; t += blockDim.x) P.tile_off[t] = s_tot[t];
+    if (threadIdx.x == 0) P.tile_off[T] = ta;
 }
 
 // --------------------------------------------------------------------------- k_emit

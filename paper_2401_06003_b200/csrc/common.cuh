@@ -15,13 +15,10 @@ constexpr int kTile = 16;                 // pyramid tiles are 16 x 16 pixels
 constexpr int kTilePix = kTile * kTile;   // one CTA thread per tile pixel
 constexpr int kCap = 16;                  // "clamped to a maximum size of 16"
 constexpr int kMaxLayers = 16;
-#ifndef TRIPS_DENSE_KEPT
-#define TRIPS_DENSE_KEPT 1
-#endif
-// Kept lists stored dense per tile, [tile][m][pixel] (16 slots per pixel, 4096 per tile), so that
-// a warp's m-th entries are contiguous: the raster stores and the backward loads of keys and
-// gamma coalesce.  0 = compact per-pixel runs (scan of K per tile; experiment builds only).
-constexpr bool kDenseKept = TRIPS_DENSE_KEPT != 0;
+// Kept lists are stored dense per tile, [tile][m][pixel] (16 slots per pixel, 4096 per tile), so
+// that a warp's m-th entries are contiguous: the raster stores and the backward loads of keys and
+// gamma coalesce (compact per-pixel runs were measured 14% slower in k_raster).
+__host__ __device__ constexpr size_t kept_base(int t) { return (size_t)t * kTilePix * kCap; }
 
 constexpr float kEps = 0.25f;             // "at least eps = 0.25"
 constexpr uint64_t kKeyMax = ~0ull;
@@ -63,15 +60,14 @@ struct Params {
     uint32_t* hist;        // [C][T]   per-CTA tile counts -> per-CTA offsets within the tile
     uint32_t* cta_vis;     // [C]      visible points per binning CTA (statistics)
     uint32_t* tile_off;    // [T+1]    first pair of each tile's bin; [T] = number of pairs M
-    uint32_t* tile_kbase;  // [T+1]    kept-list base per tile (4096 t when dense, else scan of min(4096, 4 cnt))
     uint64_t* bin_key;     // [8n]     (z bits << 32 | i) per (tile, pair), tile-major
     uint16_t* bin_orig;    // [8n]     footprint origin in the tile: (qx0+1) | (qy0+1) << 5
     uint32_t* pix_cnt;     // [T*256]  list length per tile pixel
-    uint32_t* pix_meta;    // [T*256]  (local kept offset << 5) | K
-    uint64_t* kept;        // [kcap]   kept (z, i) keys in blend order, dense [tile][m][pixel]; with
+    uint32_t* pix_meta;    // [T*256]  K (kept-list length; T_min: the cut length)
+    uint64_t* kept;        // [T*4096] kept (z, i) keys in blend order, [tile][m][pixel]; with
                            //          coarse inclusion (z, i << 4 | d)
     uint64_t* own;         // [T][16][256] coarse inclusion only: each pixel's own sorted top-16
-    float* kept_gamma;     // [kcap]   gamma of each kept fragment (saved for the backward)
+    float* kept_gamma;     // [T*4096] gamma of each kept fragment (saved for the backward)
     unsigned long long* stats;  // [8]  n_culled, n_visible, n_pairs, n_frag, n_kept, n_trunc, max_list
 };
 

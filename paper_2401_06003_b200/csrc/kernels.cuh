@@ -324,14 +324,9 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
     // Record gathers are issued kBatch at a time.  Without a following backward the loop
     // stops once T == 0 exactly (later terms vanish); with one, every gamma_m is needed.
     const int K = valid ? (int)min(total, (uint32_t)kCap) : 0;
-    uint32_t koff = (uint32_t)tid;                   // dense [tile][m][pixel]: entry m at kidx + m * KS
-    if constexpr (!kDenseKept) {
-        uint32_t ktot;
-        koff = block_excl_scan((uint32_t)K, s_warp, &ktot);
-    }
-    constexpr int KS = kDenseKept ? kTilePix : 1;
+    constexpr int KS = kTilePix;                     // [tile][m][pixel]: entry m at kidx + m * KS
     TRIPS_PCLK(4);
-    const size_t kidx = (size_t)P.tile_kbase[t] + koff;
+    const size_t kidx = kept_base(t) + (size_t)tid;
     float C[FC];
 #pragma unroll
     for (int c = 0; c < FC; ++c) C[c] = 0.f;
@@ -382,7 +377,7 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
 
     // phase E: store the sorted kept lists and per-pixel metadata
     P.pix_cnt[(size_t)t * kTilePix + tid] = valid ? total : 0u;
-    P.pix_meta[(size_t)t * kTilePix + tid] = (koff << 5) | (uint32_t)Keff;
+    P.pix_meta[(size_t)t * kTilePix + tid] = (uint32_t)Keff;
     if (save) {
         uint64_t* kp = P.kept + kidx;
 #pragma unroll
@@ -400,7 +395,7 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
 // order by (z, i, d) -- the same point's fragment in a finer layer first (i < 2^28 by the plan
 // limit).  The top-16 of a union is inside the union of the top-16s, so the own lists suffice.
 // Then the front-to-back blend of k_raster phase D, each fragment weighted in its own layer and
-// pixel; kept lists are dense (16 per pixel, tile_kbase[t] = 4096 t).
+// pixel; kept lists [tile][m][pixel] as in k_raster.
 template <int FC>
 __global__ void __launch_bounds__(kTilePix) k_coarse_blend(Params P, float* __restrict__ pyramid, int save)
 {
@@ -436,7 +431,7 @@ __global__ void __launch_bounds__(kTilePix) k_coarse_blend(Params P, float* __re
     K = min(K, kCap);
 
     // dense kept lists, [tile][m][pixel] (stride kTilePix between a pixel's entries)
-    const size_t kidx = (size_t)P.tile_kbase[t] + (size_t)tid;
+    const size_t kidx = kept_base(t) + (size_t)tid;
     float C[FC];
 #pragma unroll
     for (int c = 0; c < FC; ++c) C[c] = 0.f;
@@ -482,7 +477,7 @@ __global__ void __launch_bounds__(kTilePix) k_coarse_blend(Params P, float* __re
             if (c < P.F) out[c * plane] = C[c];
         out[P.F * plane] = A;
     }
-    P.pix_meta[(size_t)t * kTilePix + tid] = ((uint32_t)tid << 5) | (uint32_t)Keff;
+    P.pix_meta[(size_t)t * kTilePix + tid] = (uint32_t)Keff;
     if (save) {
         uint64_t* kp = P.kept + kidx;
 #pragma unroll
@@ -553,10 +548,10 @@ __global__ void __launch_bounds__(kTilePix, FC <= 4 ? TRIPS_BWD_CTAS : 2) k_back
     const uint32_t meta = P.pix_meta[(size_t)t * kTilePix + tid];
     const int K = (int)(meta & 31u);
     if (!CAM && K == 0) return;
-    const size_t kidx = (size_t)P.tile_kbase[t] + (meta >> 5);
+    const size_t kidx = kept_base(t) + (size_t)tid;
     const uint64_t* kp = P.kept + kidx;
     const float* gm = P.kept_gamma + kidx;
-    constexpr int KS = (COARSE || kDenseKept) ? kTilePix : 1;   // entry stride (dense: [tile][m][pixel])
+    constexpr int KS = kTilePix;                     // entry stride ([tile][m][pixel])
     float cg[CAM ? 17 : 1];
 #pragma unroll
     for (int k = 0; k < (CAM ? 17 : 1); ++k) cg[k] = 0.f;
@@ -671,10 +666,10 @@ __global__ void __launch_bounds__(kTilePix) k_export(Params P, int what, void* d
     } else {
         const uint32_t meta = P.pix_meta[(size_t)t * kTilePix + tid];
         const int K = (int)(meta & 31u);
-        const uint64_t* kp = P.kept + P.tile_kbase[t] + (meta >> 5);
+        const uint64_t* kp = P.kept + kept_base(t) + tid;
         int32_t* o = static_cast<int32_t*>(dst) + pidx * kCap;
         for (int m = 0; m < kCap; ++m) {
-            const uint32_t lo = (uint32_t)kp[(kDenseKept || P.coarse) ? m * kTilePix : m];
+            const uint32_t lo = (uint32_t)kp[m * kTilePix];
             if (what == 3) o[m] = m < K ? (P.coarse ? (int32_t)(lo & 15u) : 0) : -1;
             else o[m] = m < K ? (int32_t)(P.coarse ? lo >> 4 : lo) : -1;
         }

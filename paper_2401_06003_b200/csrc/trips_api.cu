@@ -40,7 +40,7 @@ struct trips_plan {
     uint64_t kcap;
     // workspace layout (byte offsets)
     int32_t ctas;           // binning CTAs (persistent grid)
-    size_t off_geo, off_tau, off_z, off_hist, off_cvis, off_toff, off_tkb, off_bkey, off_borig, off_pcnt, off_pmeta, off_kept, off_kgam,
+    size_t off_geo, off_tau, off_z, off_hist, off_cvis, off_toff, off_bkey, off_borig, off_pcnt, off_pmeta, off_kept, off_kgam,
         off_own, off_stats, ws_bytes;
     // state
     const void* ws_bound = nullptr;
@@ -127,6 +127,7 @@ int set_smem_attrs(size_t bytes)
     if (bytes <= done) return TRIPS_OK;
     cudaError_t e = cudaFuncSetAttribute(k_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     int bad = (int)e;
+    bad |= (int)cudaFuncSetAttribute(k_tscan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     bad |= set_emit_attr<4>(bytes) | set_emit_attr<8>(bytes) | set_emit_attr<12>(bytes) | set_emit_attr<16>(bytes) |
            set_emit_attr<20>(bytes) | set_emit_attr<24>(bytes) | set_emit_attr<28>(bytes) | set_emit_attr<32>(bytes);
     if (bad) return cuda_status(cudaGetLastError());
@@ -160,7 +161,6 @@ Params make_params(const trips_plan* p, void* ws)
     P.hist = reinterpret_cast<uint32_t*>(b + p->off_hist);
     P.cta_vis = reinterpret_cast<uint32_t*>(b + p->off_cvis);
     P.tile_off = reinterpret_cast<uint32_t*>(b + p->off_toff);
-    P.tile_kbase = reinterpret_cast<uint32_t*>(b + p->off_tkb);
     P.bin_key = reinterpret_cast<uint64_t*>(b + p->off_bkey);
     P.bin_orig = reinterpret_cast<uint16_t*>(b + p->off_borig);
     P.pix_cnt = reinterpret_cast<uint32_t*>(b + p->off_pcnt);
@@ -225,8 +225,7 @@ int trips_plan_create(const trips_config* cfg, int32_t width, int32_t height, in
     p->P = pix;
     p->T = tiles;
     p->pyr_floats = pix * (F + 1);
-    const uint64_t kc1 = (uint64_t)tiles * kTilePix * kCap, kc2 = (uint64_t)max_points * 32;
-    p->kcap = (kDenseKept || p->coarse || kc1 < kc2) ? kc1 : kc2;    // dense: 16 slots per pixel
+    p->kcap = (uint64_t)tiles * kTilePix * kCap;       // kept lists: 16 slots per tile pixel
     if (p->kcap >= (uint64_t(1) << 32) || tiles > kMaxTilesSmem) { delete p; return TRIPS_ERR_ARG; }
     const size_t N = (size_t)(max_points > 0 ? max_points : 1);
     size_t o = 0;
@@ -237,7 +236,6 @@ int trips_plan_create(const trips_config* cfg, int32_t width, int32_t height, in
     p->off_hist = o;   o = align256(o + (size_t)p->ctas * tiles * 4);
     p->off_cvis = o;   o = align256(o + (size_t)p->ctas * 4);
     p->off_toff = o;   o = align256(o + ((size_t)tiles + 1) * 4);
-    p->off_tkb = o;    o = align256(o + ((size_t)tiles + 1) * 4);
     p->off_bkey = o;   o = align256(o + 8 * N * 8);
     p->off_borig = o;  o = align256(o + 8 * N * 2);
     p->off_pcnt = o;  o = align256(o + (size_t)tiles * kTilePix * 4);
@@ -313,7 +311,7 @@ int trips_project(trips_plan* p, void* ws, const trips_camera* c, int64_t n, con
         StageScope sc(p, 0, st);
         TRIPS_FC_SWITCH(p->FC, (k_count<kFC><<<p->ctas, kBinThreads, hsm, st>>>(P, level_out, proj_out)));
         if ((rc = check_launch())) return rc;
-        k_tscan<<<1, 1024, 0, st>>>(P);
+        k_tscan<<<1, 1024, hsm, st>>>(P);
         if ((rc = check_launch())) return rc;
     }
     {
