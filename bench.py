@@ -411,6 +411,12 @@ def run_cuda(args, rank, world, local_rank):
                     "d2h_bytes_per_step": d2h},
             "view_stats_mean": {k: float(np.mean([s[k] for s in view_stats])) for k in view_stats[0]},
         }
+        alone_ms = (variants.get("plain") or {}).get(dom)
+        if alone_ms:
+            # the same kernel timed alone on one stream (side measurement, CUDA events on its
+            # stream): its own roofline fraction without the other stream's kernels sharing the SMs
+            line["roofline"]["alone"] = {"launch_ms": alone_ms, "achieved": dom_bytes / (alone_ms * 1e-3) / 1e9,
+                                         "frac": dom_bytes / (alone_ms * 1e-3) / 1e9 / peak}
         if clk is not None:
             line["clocks"] = clk
         if random_order is not None:

@@ -139,7 +139,8 @@ __global__ void __launch_bounds__(kBinThreads) k_count(Params P, int8_t* __restr
 #else
     const int rot = 0;
 #endif
-    for (int k = threadIdx.x; k < P.T; k += blockDim.x) {
+#pragma unroll 8
+    for (int k = threadIdx.x; k < P.T; k += blockDim.x) {      // unrolled: 8 atomics in flight
         int t = k + rot;
         if (t >= P.T) t -= P.T;
         const uint32_t c = s_hist[t];
@@ -187,6 +188,7 @@ __global__ void __launch_bounds__(kBinThreads, kBinCtasPerSm) k_emit(Params P)
     extern __shared__ __align__(16) uint32_t s_cur[];             // [T] fill cursors
     const uint32_t* row = P.hist + (size_t)blockIdx.x * P.T;
     // entries of tiles this CTA never touches are garbage and never used
+#pragma unroll 8
     for (int t = threadIdx.x; t < P.T; t += blockDim.x) s_cur[t] = P.tile_off[t] + row[t];
     __syncthreads();
     int b, e;
