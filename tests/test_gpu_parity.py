@@ -36,12 +36,18 @@ def _ovar(var):
     return dict(t_min=var.get("t_min", 0.0), coarse=var.get("coarse_layers", 0))
 
 
-def gpu_run(sc, dev, cam=None, G=None, save=True, export=True, **var):
-    """var: Rasterizer variant options (t_min, coarse_layers)."""
+def gpu_run(sc, dev, cam=None, G=None, save=True, export=True, desc_misalign=False, **var):
+    """var: Rasterizer variant options (t_min, coarse_layers).  desc_misalign: pass the descriptors
+    as a view 4 bytes into a buffer (4-B but not 16-B aligned: the library takes its padded copy)."""
     from paper_2401_06003_b200 import Rasterizer
     cam = cam or sc.cams[0]
     r = Rasterizer(cam.width, cam.height, sc.n_layers, sc.F, max_points=max(sc.n, 1), device=dev, **var)
     pos, sw, al, de = (T(a, dev) for a in (sc.pos, sc.sw, sc.alpha, sc.desc))
+    if desc_misalign:
+        buf = torch.zeros(de.numel() + 4, dtype=torch.float32, device=dev)
+        de = buf[1:1 + de.numel()].view(sc.n, sc.F)
+        de.copy_(T(sc.desc, dev))
+        assert de.data_ptr() % 16 != 0
     level = torch.empty(sc.n, dtype=torch.int8, device=dev)
     proj = torch.empty(sc.n, 4, dtype=torch.float32, device=dev)
     r.project(cam, pos, sw, al, de, level_out=level, proj_out=proj)
@@ -164,6 +170,17 @@ def test_feature_counts(dev, F):
     sc = scenes.tiny_scene(3, n=500, F=F, W=50, H=37, n_layers=4)
     G = grads_for(sc, sc.cams[0], seed=F)
     got = gpu_run(sc, dev, G=G)
+    check_forward(sc, got)
+    check_backward(sc, got, G)
+
+
+@pytest.mark.parametrize("F", [4, 8])
+def test_descriptors_not_16b_aligned(dev, F):
+    # F % 4 == 0 but desc only 4-B aligned: the padded workspace copy is gathered instead of the
+    # caller's rows (include/trips.h, trips_project)
+    sc = scenes.tiny_scene(7, n=600, F=F, W=61, H=45, n_layers=4)
+    G = grads_for(sc, sc.cams[0], seed=F + 50)
+    got = gpu_run(sc, dev, G=G, desc_misalign=True)
     check_forward(sc, got)
     check_backward(sc, got, G)
 
