@@ -24,6 +24,9 @@ namespace trips {
 #ifndef TRIPS_RASTER_CTAS
 #define TRIPS_RASTER_CTAS 3
 #endif
+#ifndef TRIPS_THR_SKIP0
+#define TRIPS_THR_SKIP0 1
+#endif
 #ifndef TRIPS_BWD_CTAS
 #define TRIPS_BWD_CTAS 3
 #endif
@@ -110,6 +113,26 @@ __device__ __forceinline__ void merge_keep16(uint64_t (&r)[16], const uint64_t (
 #pragma unroll
         for (int i = 0; i < 16; ++i)
             if ((i & d) == 0) cswap(r[i], r[i + d]);
+}
+
+// Exclusive prefix of one u32 per thread over a 256-thread tile CTA with a single barrier:
+// warp-inclusive shuffle scan, warp totals through shared memory, each thread adds the totals of
+// the warps before it.  `s_warp` (>= 8 u32) must not be rewritten before the next barrier.
+__device__ __forceinline__ uint32_t tile_excl_scan(uint32_t v, uint32_t* s_warp)
+{
+    const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= (unsigned)o) x += y;
+    }
+    if (lane == 31) s_warp[warp] = x;
+    __syncthreads();
+    uint32_t pre = 0;
+#pragma unroll
+    for (int w = 0; w < kTilePix / 32 - 1; ++w) pre += (w < (int)warp) ? s_warp[w] : 0u;
+    return pre + x - v;
 }
 
 // --------------------------------------------------------------------------- fragment weights
@@ -240,7 +263,11 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
                 for (int c = 0; c < 4; ++c) {
                     if (o & (1u << (10 + c))) {               // corner inside this tile and layer
                         const uint32_t q = (uint32_t)(q0 + (c & 1) + (c >> 1) * kTile);
-                        if (key >= s_thr[q]) {
+                        if (TRIPS_THR_SKIP0 && ch == 0) {
+                            // first chunk: no pixel holds 16 keys yet, nothing can be rejected
+                            const uint32_t rank = atomicAdd(&s_cnt[q], 1u);
+                            fq[k][c] = q | (rank << 8);
+                        } else if (key >= s_thr[q]) {
                             // cannot enter this pixel's top-16 any more (keys are unique):
                             // counted for the list length, never sorted
                             atomicAdd(&s_rej[q], 1u);
@@ -254,9 +281,8 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
         }
         __syncthreads();
         TRIPS_PCLK(0);
-        uint32_t chunk_total;
         const uint32_t my_cnt = s_cnt[tid];
-        const uint32_t my_base = block_excl_scan(my_cnt, s_warp, &chunk_total);
+        const uint32_t my_base = tile_excl_scan(my_cnt, s_warp);
         s_base[tid] = my_base;
         __syncthreads();
         TRIPS_PCLK(1);
@@ -305,7 +331,7 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
         }
         total += my_cnt + s_rej[tid];
         s_thr[tid] = r[15];                          // 16th smallest key so far (MAX if < 16)
-        __syncthreads();
+        if (ch + 1 < nch) __syncthreads();           // shared buffers are reused by the next chunk only
         TRIPS_PCLK(3);
     }
 
