@@ -23,7 +23,10 @@
 namespace trips {
 
 constexpr int kBinThreads = 512;           // threads per binning CTA
-constexpr int kBinCtasPerSm = 3;
+#ifndef TRIPS_BIN_CTAS
+#define TRIPS_BIN_CTAS 3
+#endif
+constexpr int kBinCtasPerSm = TRIPS_BIN_CTAS;
 constexpr int kMaxTilesSmem = 49152;       // 192 KB of shared-memory counters
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
@@ -70,7 +73,7 @@ __device__ __forceinline__ void cta_range(int n, int& b, int& e)
 // Projects every point once (exact block), writes its screen record and depth, and counts its
 // (point, tile) pairs in shared-memory counters.
 template <int FC>
-__global__ void __launch_bounds__(kBinThreads) k_count(Params P, int8_t* __restrict__ level_out,
+__global__ void __launch_bounds__(kBinThreads, kBinCtasPerSm) k_count(Params P, int8_t* __restrict__ level_out,
                                                        float* __restrict__ proj_out)
 {
     extern __shared__ __align__(16) uint32_t s_hist[];            // [T]
