@@ -71,8 +71,9 @@ typedef struct {
                                   d = 0 .. min(c, n - 1 - l), ordered by (z, i, d); each
                                   fragment keeps its own gamma (Eq. 3 in its own layer).
                                   Per-pixel counts and stats stay the pixel's own list.  Costs
-                                  an extra 16 keys per pyramid pixel of workspace (dense kept
-                                  lists).  c > n - 1 behaves as n - 1; c < 0 is an error. */
+                                  an extra 16 keys per pyramid pixel of workspace (each pixel's
+                                  own sorted list).  c > n - 1 behaves as n - 1; c < 0 is an
+                                  error. */
 } trips_config;
 
 typedef struct trips_plan trips_plan;   /* opaque, host memory, owned by the library */
