@@ -87,9 +87,33 @@ __global__ void __launch_bounds__(kBinThreads, kBinCtasPerSm) k_count(Params P, 
 #ifndef TRIPS_COUNT_UNROLL
 #define TRIPS_COUNT_UNROLL 1
 #endif
+#ifndef TRIPS_COUNT_PREFETCH
+#define TRIPS_COUNT_PREFETCH 1
+#endif
     constexpr int kU = TRIPS_COUNT_UNROLL;        // points per thread per iteration (loads issued together)
+#if TRIPS_COUNT_PREFETCH
+    // the next point's inputs are loaded while this one is projected and counted
+    float nx[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
+    if (b + (int)threadIdx.x < e) {
+        const int i = b + threadIdx.x;
+        const float* q = P.pos + 3 * (size_t)i;
+        nx[0] = __ldg(q); nx[1] = __ldg(q + 1); nx[2] = __ldg(q + 2); nx[3] = __ldg(P.sw + i); nx[4] = __ldg(P.alpha + i);
+    }
+#endif
     for (int i0 = b + threadIdx.x; i0 < e; i0 += kU * blockDim.x) {
       float in[kU][5];
+#if TRIPS_COUNT_PREFETCH
+      static_assert(kU == 1, "prefetch assumes one point per iteration");
+#pragma unroll
+      for (int k = 0; k < 5; ++k) in[0][k] = nx[k];
+      {
+        const int i = i0 + (int)blockDim.x;
+        if (i < e) {
+            const float* q = P.pos + 3 * (size_t)i;
+            nx[0] = __ldg(q); nx[1] = __ldg(q + 1); nx[2] = __ldg(q + 2); nx[3] = __ldg(P.sw + i); nx[4] = __ldg(P.alpha + i);
+        }
+      }
+#else
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
         const int i = min(i0 + u * (int)blockDim.x, e - 1);
@@ -97,6 +121,7 @@ __global__ void __launch_bounds__(kBinThreads, kBinCtasPerSm) k_count(Params P, 
         in[u][0] = __ldg(q); in[u][1] = __ldg(q + 1); in[u][2] = __ldg(q + 2);
         in[u][3] = __ldg(P.sw + i); in[u][4] = __ldg(P.alpha + i);
       }
+#endif
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
         const int i = i0 + u * (int)blockDim.x;
