@@ -47,7 +47,8 @@ def build(force=False, verbose=False, out=None, extra=()):
         sys.stderr.write(res.stderr)
     if out == LIB:
         with open(os.path.join(CSRC, "ptxas_info.txt"), "w") as f:
-            f.write(res.stderr)
+            # registers / spills / shared memory per kernel; compile times dropped (not reproducible)
+            f.write("".join(l for l in res.stderr.splitlines(True) if "Compile time" not in l))
     os.replace(tmp, out)
     return out
 
