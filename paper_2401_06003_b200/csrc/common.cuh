@@ -221,6 +221,9 @@ __device__ __forceinline__ int pair_slot(const Params& P, const PointPairs& pp, 
 // ((qx0 + 1) | (qy0 + 1) << 5) and, in bits 10-13, which of the 4 corners (c = dx + 2 dy) are
 // pixels of this tile inside the layer -- computed here, in the memory-bound binning pass,
 // instead of per pair in the ALU-bound raster kernel.
+#ifndef TRIPS_PAIR_UNROLL
+#define TRIPS_PAIR_UNROLL 1
+#endif
 template <class Fn>
 __device__ __forceinline__ void for_each_pair(const Params& P, float xs, float ys, float s, Fn&& fn)
 {
@@ -233,8 +236,19 @@ __device__ __forceinline__ void for_each_pair(const Params& P, float xs, float y
         const int xa = max(f.x0, 0), xb = min(f.x0 + 1, G.W - 1);
         const int ya = max(f.y0, 0), yb = min(f.y0 + 1, G.H - 1);
         if (xa > xb || ya > yb) continue;
+#if TRIPS_PAIR_UNROLL
+        // a footprint spans at most 2 x 2 tiles: fixed-trip loops, predicated
+        const int ty0 = ya >> 4, tx0 = xa >> 4, ny = (yb >> 4) - ty0, nx = (xb >> 4) - tx0;
+#pragma unroll
+        for (int dy = 0; dy < 2; ++dy)
+#pragma unroll
+            for (int dx = 0; dx < 2; ++dx) {
+                if (dy > ny || dx > nx) continue;
+                const int ty = ty0 + dy, tx = tx0 + dx;
+#else
         for (int ty = ya >> 4; ty <= (yb >> 4); ++ty)
             for (int tx = xa >> 4; tx <= (xb >> 4); ++tx) {
+#endif
                 // columns / rows of the footprint inside [xa, xb] and this tile (separable)
                 const int cxa = max(xa, tx * 16), cxb = min(xb, tx * 16 + 15);
                 const int cya = max(ya, ty * 16), cyb = min(yb, ty * 16 + 15);
