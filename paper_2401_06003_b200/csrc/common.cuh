@@ -222,13 +222,19 @@ __device__ __forceinline__ int pair_slot(const Params& P, const PointPairs& pp, 
 // pixels of this tile inside the layer -- computed here, in the memory-bound binning pass,
 // instead of per pair in the ALU-bound raster kernel.
 #ifndef TRIPS_PAIR_UNROLL
-#define TRIPS_PAIR_UNROLL 1
+#define TRIPS_PAIR_UNROLL 2
 #endif
 template <class Fn>
 __device__ __forceinline__ void for_each_pair(const Params& P, float xs, float ys, float s, Fn&& fn)
 {
     const Levels lv = select_levels(s, P.n_layers);
+#if TRIPS_PAIR_UNROLL >= 2
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        if (k >= lv.n) break;
+#else
     for (int k = 0; k < lv.n; ++k) {
+#endif
         const int l = lv.lo + k;
         const LayerGeom& G = P.L[l];
         Foot f;
@@ -237,7 +243,7 @@ __device__ __forceinline__ void for_each_pair(const Params& P, float xs, float y
         const int ya = max(f.y0, 0), yb = min(f.y0 + 1, G.H - 1);
         if (xa > xb || ya > yb) continue;
 #if TRIPS_PAIR_UNROLL
-        // a footprint spans at most 2 x 2 tiles: fixed-trip loops, predicated
+        // a footprint spans at most 2 x 2 tiles: fixed-trip loops, predicated (as the layer loop)
         const int ty0 = ya >> 4, tx0 = xa >> 4, ny = (yb >> 4) - ty0, nx = (xb >> 4) - tx0;
 #pragma unroll
         for (int dy = 0; dy < 2; ++dy)
