@@ -103,6 +103,9 @@ __device__ __forceinline__ bool project_exact(const Cam& c, float X, float Y, fl
 // Layer selection, readings Q1-Q5.  Returns the number of layers (1/2),
 // the lowest layer, the weights iota[2] and d iota / d s (right derivative at kinks, Q19).
 // Level code: bits 0-3 lowest layer, 0x10 two layers, 0x20 eps branch, 0x40 clamp.
+#ifndef TRIPS_LEVELS_SELECT
+#define TRIPS_LEVELS_SELECT 1
+#endif
 struct Levels {
     int n, lo, code;
     float iota[2];
@@ -111,6 +114,28 @@ struct Levels {
 
 __device__ __forceinline__ Levels select_levels(float s, int n_layers)
 {
+#if TRIPS_LEVELS_SELECT
+    // branch-free form of the same cases (selects instead of divergent branches; identical values)
+    {
+        Levels L;
+        const bool eps = s < 1.0f;
+        const uint32_t bits = __float_as_uint(s);
+        const int k = (int)(bits >> 23) - 127;
+        const bool clamp = !eps && k >= n_layers - 1;
+        const float m = __uint_as_float((bits & 0x007FFFFFu) | 0x3F800000u);
+        const float inv = __uint_as_float((uint32_t)(127 - min(max(k, -126), 126)) << 23);
+        const bool p2 = !eps && !clamp && m == 1.0f;
+        const bool one = eps || clamp || p2;
+        L.n = one ? 1 : 2;
+        L.lo = eps ? 0 : (clamp ? n_layers - 1 : k);
+        L.code = eps ? 0x20 : (clamp ? (0x40 | (n_layers - 1)) : (p2 ? k : (0x10 | k)));
+        L.iota[0] = eps ? __fadd_rn(kEps, __fmul_rn(1.0f - kEps, s)) : ((clamp || p2) ? 1.0f : __fsub_rn(2.0f, m));
+        L.iota[1] = one ? 0.0f : __fsub_rn(m, 1.0f);
+        L.diota[0] = eps ? 1.0f - kEps : (clamp ? 0.0f : -inv);
+        L.diota[1] = one ? 0.0f : inv;
+        return L;
+    }
+#endif
     Levels L;
     if (s < 1.0f) {                                  // second case of Eq. (4), reading Q3
         L.n = 1; L.lo = 0; L.code = 0x20;
