@@ -42,6 +42,8 @@ def _lib(real: str):
                                         vp, vp, vp, vp, vp, vp]
         lib.oracle_set_t_min.restype = None
         lib.oracle_set_t_min.argtypes = [C.c_float]
+        lib.oracle_set_screen_out.restype = None
+        lib.oracle_set_screen_out.argtypes = [vp, vp]
         lib.oracle_set_coarse.restype = None
         lib.oracle_set_coarse.argtypes = [C.c_int, vp]
         lib.oracle_knn4.restype = C.c_int
@@ -179,19 +181,25 @@ CAMERA_GRAD_NAMES = ("R00", "R01", "R02", "R10", "R11", "R12", "R20", "R21", "R2
 
 
 def backward(cam, n_layers, pos, sw, alpha, desc, grad_pyramid, mask=None, real="float", grad=None,
-             grad_mag=None, grad_cam=None, grad_cam_mag=None, t_min=0.0, coarse=0):
+             grad_mag=None, grad_cam=None, grad_cam_mag=None, t_min=0.0, coarse=0, screen=None, screen_mag=None):
     """O1 backward.  Returns (grad [n, 5+F] float64, grad_mag [n, 5+F]); rows are
     (d/dx, d/dy, d/dz, d/ds_w, d/dalpha, d/dtau[F]).  If grad / grad_mag are given
     they are accumulated into (multi-view sum, reading Q21).  grad_cam / grad_cam_mag
-    (float64 [17], CAMERA_GRAD_NAMES order) receive the camera gradient if given."""
+    (float64 [17], CAMERA_GRAD_NAMES order) receive the camera gradient if given.
+    screen / screen_mag (float64 [n, 4+F], overwritten) receive the screen-space gradients
+    (d/dx, d/dy, d/ds, d/dalpha, d/dtau) and their magnitudes if given."""
     _lib(real).oracle_set_t_min(float(np.float32(t_min)))
     _lib(real).oracle_set_coarse(int(coarse), None)
+    for a in (screen, screen_mag):
+        assert a is None or (a.dtype == np.float64 and a.flags.c_contiguous)
+    _lib(real).oracle_set_screen_out(_ptr(screen), _ptr(screen_mag))
     try:
         return _backward(cam, n_layers, pos, sw, alpha, desc, grad_pyramid, mask, real, grad, grad_mag, grad_cam,
                          grad_cam_mag)
     finally:
         _lib(real).oracle_set_t_min(0.0)
         _lib(real).oracle_set_coarse(0, None)
+        _lib(real).oracle_set_screen_out(None, None)
 
 
 def _backward(cam, n_layers, pos, sw, alpha, desc, grad_pyramid, mask, real, grad, grad_mag, grad_cam,

@@ -151,11 +151,10 @@ static int select_layers(real s, int n_layers, int layer[2], real iota[2], doubl
     return 2;
 }
 
-/* One footprint pixel of Eq. (3) (Q7, Q9). */
+/* One footprint pixel of Eq. (3) (Q7, Q9); its weights are evaluated by frag_weights(). */
 typedef struct {
     int32_t px, py;             /* pixel in layer l */
     int dx, dy;                 /* which corner of the 2x2 footprint */
-    real wx, wy, beta;
 } corner_t;
 
 /* Enumerates the in-bounds pixels of the 2x2 footprint in layer l.  Returns count. */
@@ -165,7 +164,6 @@ static int footprint(real xs, real ys, int l, int32_t Wl, int32_t Hl, corner_t o
     real xl = xs * scale, yl = ys * scale;
     if (!(xl >= (real)-1 && xl < (real)Wl && yl >= (real)-1 && yl < (real)Hl)) return 0;
     real x0 = floor(xl), y0 = floor(yl);
-    real fx = xl - x0, fy = yl - y0;
     int cnt = 0;
     for (int dy = 0; dy < 2; ++dy)
         for (int dx = 0; dx < 2; ++dx) {
@@ -173,9 +171,6 @@ static int footprint(real xs, real ys, int l, int32_t Wl, int32_t Hl, corner_t o
             if (px < 0 || px >= Wl || py < 0 || py >= Hl) continue;
             corner_t* c = &out[cnt++];
             c->px = px; c->py = py; c->dx = dx; c->dy = dy;
-            c->wx = dx ? fx : (real)1 - fx;                  /* 1 - |x - x_i| */
-            c->wy = dy ? fy : (real)1 - fy;
-            c->beta = c->wx * c->wy;
         }
     return cnt;
 }
@@ -503,6 +498,14 @@ int oracle_forward(const oracle_camera* cam, int n_layers, int F, int64_t n, con
 
 /* ---------------------------------------------------------------- backward */
 
+/* Optional export of the per-point screen-space gradients of the last oracle_backward call
+ * (SURVEY.md 8(b) SCREEN_GRADS): [n][4+F] doubles (d/dx, d/dy, d/ds in layer-0 pixels, d/dalpha,
+ * d/dtau[F]) -- the values the projection chain below consumes -- and their |.| magnitudes. */
+static double* g_screen_out = NULL;
+static double* g_screen_mag = NULL;
+
+void oracle_set_screen_out(double* screen, double* screen_mag) { g_screen_out = screen; g_screen_mag = screen_mag; }
+
 /* Backward pass (chain rule of Eqs. 2-6; depth order and list membership held
  * constant).  Gradients w.r.t. the raw parameters (Q20), SUMMED
  * into grad (so several views can be accumulated, Q21):
@@ -664,6 +667,8 @@ int oracle_backward(const oracle_camera* cam, int n_layers, int F, int64_t n, co
             for (int c = 0; c < F; ++c) mo[5 + c] += mi[4 + c];
         }
     }
+    if (g_screen_out) memcpy(g_screen_out, gs, sizeof(double) * (size_t)n * G);
+    if (g_screen_mag) memcpy(g_screen_mag, ms, sizeof(double) * (size_t)n * G);
     free(gs); free(ms);
     free_scene(&S);
     return 0;

@@ -58,3 +58,21 @@ def test_cut_list_backward_matches_finite_differences():
         assert abs(fd - g[i, 5 + c]) <= 1e-6 * gm[i, 5 + c] + 1e-9 + 1e-6 * abs(fd)
         checked += 1
     assert checked == 40
+
+
+def test_cut_boundary_equal_transmittance_is_not_cut():
+    """Reading Q17: the kept list ends with the fragment after which T drops BELOW t_min (strict).
+    gamma = 0.5 exactly (pixel centre, s = 1, alpha = 0.5), so T = 0.5, 0.25, 0.125, ... exactly:
+    with t_min = 0.25 the second fragment leaves T == t_min (not below) and the third is kept too;
+    one ulp above 0.25 the cut falls after the second."""
+    cam = unit_cam(16, 16, f=8.0)
+    zs = 1.0 + np.arange(6) / 32.0
+    pos, sw, a, d = point_scene(cam, [[7.0, 7.0, z] for z in zs], [1.0] * 6, alpha=[0.5] * 6,
+                                desc=np.ones(6))
+    for t_min, K in ((0.25, 3), (float(np.nextafter(np.float32(0.25), np.float32(1))), 2), (0.5, 2),
+                     (float(np.nextafter(np.float32(0.5), np.float32(1))), 1)):
+        r = oracle.forward(cam, 3, pos, sw, a, d, t_min=t_min)
+        kept = oracle.split_pixels(r["kept"].reshape(-1), 16, 16, 3, 16)[0][7, 7]
+        assert list(kept[:K + 1]) == list(range(K)) + [-1], (t_min, kept[:4])
+        A = oracle.split_pyramid(r["pyramid"], 1, 16, 16, 3)[0][1, 7, 7]
+        assert A == 1.0 - 0.5 ** K                       # exact: sum_m T_m gamma_m of the kept prefix
