@@ -198,7 +198,7 @@ def run_cuda(args, rank, world, local_rank):
             for k, v in (("pos", sc.pos), ("sw", sc.sw), ("alpha", sc.alpha), ("desc", sc.desc))}
     d = {k: v.to(dev, non_blocking=True) for k, v in host.items()}
     Gp = torch.from_numpy(scenes.grad_pyramid(rast.pyramid_floats, seed=100)).to(dev)
-    grad = torch.zeros(n, rast.G, dtype=torch.float32, device=dev)
+    grad = rast.new_grad(n)
     my_views = tdist.shard_views(N_VIEWS, rank, world)
     stream = torch.cuda.current_stream()
 
@@ -298,7 +298,7 @@ def run_cuda(args, rank, world, local_rank):
     # ---- side measurement: blend variants and feature counts, per view
     def per_view_ms(r, desc, views):
         gp = torch.from_numpy(scenes.grad_pyramid(r.pyramid_floats, seed=100)).to(dev)
-        gb = torch.zeros(n, r.G, dtype=torch.float32, device=dev)
+        gb = r.new_grad(n)
         for v in views[:2]:                                          # warm-up
             r.project(sc.cams[v], d["pos"], d["sw"], d["alpha"], desc)
             r.forward(save=True)
@@ -346,7 +346,7 @@ def run_cuda(args, rank, world, local_rank):
 
     # ---- end to end through the public API: pinned host inputs in, gradients out
     # (dist.StreamedSteps: double-buffered, copies on their own streams overlap the kernels)
-    out_host = [torch.empty(n, rast.G, dtype=torch.float32).pin_memory() for _ in range(2)]
+    out_host = [torch.empty(rast.grad_floats(n), dtype=torch.float32).pin_memory() for _ in range(2)]
     h2d = sum(v.numel() * v.element_size() for v in host.values())
     d2h = out_host[0].numel() * out_host[0].element_size()
     pipe = tdist.StreamedSteps(host, grad, dev)
@@ -395,7 +395,7 @@ def run_cuda(args, rank, world, local_rank):
                        "global_batch": N_VIEWS, "points": n, "resolution": [W, H], "layers": sc.n_layers,
                        "features": F, "parallelism": f"views{world}", "point_order": args.order,
                        "streams_per_gpu": args.streams,
-                       "l2": "inputs larger than L2 (288 MB of point data, 384 MB gradients per step)"},
+                       "l2": "inputs larger than L2 (288 MB of point data, 288 MB gradients per step)"},
             "points_per_s": N_VIEWS * n / (step_ms * 1e-3),
             "fragments_per_s": sum(s["n_frag"] for s in view_stats) * world / (step_ms * 1e-3),
             "alg_GBps_step": step_bytes * world / (step_ms * 1e-3) / 1e9,

@@ -104,8 +104,13 @@ typedef enum {
 typedef enum {
     TRIPS_EXPORT_COUNTS = 1,   /* uint32[P]: per-pixel list length, pyramid pixel order     */
     TRIPS_EXPORT_KEPT = 2,     /* int32[P*16]: kept point indices in blend order, -1 padded */
-    TRIPS_EXPORT_KEPT_LAYER = 3 /* int32[P*16]: layer offset d of each kept entry (0 unless
+    TRIPS_EXPORT_KEPT_LAYER = 3, /* int32[P*16]: layer offset d of each kept entry (0 unless
                                   coarse_layers > 0), -1 padded */
+    TRIPS_EXPORT_SCREEN_GRADS = 4 /* float[n][4+F]: screen-space gradients of the last
+                                  trips_splat_backward's grad_pyramid:
+                                  (dL/dx, dL/dy, dL/ds in layer-0 pixels, dL/dalpha, dL/dtau[F])
+                                  of this view, before the projection chain.  The caller keeps
+                                  that grad_pyramid unchanged until the export. */
 } trips_export;
 
 /* ---- plan ------------------------------------------------------------------------- */
@@ -131,10 +136,6 @@ int64_t trips_pyramid_floats(const trips_plan* plan);
  * pyramid.  Any output pointer may be NULL.  Errors: TRIPS_ERR_ARG (l out of range). */
 int trips_layer_dims(const trips_plan* plan, int32_t l, int32_t* h, int32_t* w,
                      int64_t* offset_floats);
-
-/* Row stride G (floats) of the packed gradient buffer: G = 8 + 4*ceil(F/4).  Row i holds
- * (dL/dx, dL/dy, dL/dz, dL/ds_w, dL/dalpha, dL/dtau[0..F-1], zero padding). */
-int32_t trips_grad_stride(const trips_plan* plan);
 
 /* ---- the three stages -------------------------------------------------------------- */
 
@@ -166,17 +167,30 @@ int trips_project(trips_plan* plan, void* ws, const trips_camera* cam, int64_t n
  * TRIPS_ERR_ALIGN, TRIPS_ERR_CUDA. */
 int trips_splat_forward(trips_plan* plan, void* ws, float* pyramid, uint32_t flags, void* stream);
 
-/* Backward of the last saved forward.  grad_pyramid has the pyramid layout (16-B aligned).
- * Gradients are ACCUMULATED (+=) into grad[n][G] (G = trips_grad_stride, 16-B aligned),
- * so several views sum into one buffer (reading Q21); the caller zeroes it once per batch.
+/* Backward of the last saved forward: gradients w.r.t. positions, world sizes, opacities and
+ * descriptors (chain rule of Eqs. 2-6, sorted lists reused).
+ * grad_pyramid has the pyramid layout (16-B aligned).  Gradients are ACCUMULATED (+=) so that
+ * several views sum into one set of buffers (reading Q21); the caller zeroes them once per batch:
+ *   grad_pos_size  float[n][4]  (dL/dx, dL/dy, dL/dz, dL/ds_w) per point, 16-B aligned.  Position
+ *                               and world size share one 16-byte row so that one vector reduction
+ *                               carries both (SURVEY.md 8(b) lists them as two arrays; DESIGN.md
+ *                               "Boundary" records this and the other deviations)
+ *   grad_opacity   float[n]     dL/dalpha, 4-B aligned
+ *   grad_desc      float[n][F]  dL/dtau, row-major, 4-B aligned (16-B aligned rows with F % 4 == 0
+ *                               use 16-byte vector reductions)
+ * Laid out contiguously ([4n | F n | n] floats) the three form one (5+F) n-float buffer -- 36 B
+ * per point at F = 4 -- that a multi-GPU caller all-reduces once per batch.
  * grad_camera (nullable, device float[17], 4-B aligned) receives += the gradient w.r.t. the
  * camera of the last trips_project (the paper optimises camera parameters):
  * (dR00..dR22 row-major, dt0..dt2, dfx, dfy, dcx, dcy, df) for p = R x + t, x = fx p_x/z + cx,
  * y = fy p_y/z + cy, s = f s_w/z.  Passing NULL costs nothing.
- * May be called more than once per forward.  Errors: TRIPS_ERR_STATE (last forward not
- * saved, or ws differs), TRIPS_ERR_ARG, TRIPS_ERR_ALIGN, TRIPS_ERR_CUDA. */
-int trips_splat_backward(trips_plan* plan, void* ws, const float* grad_pyramid, float* grad,
-                         float* grad_camera, void* stream);
+ * Summation order: fragments of different pixels reduce into a point's row with float atomics
+ * (red.global.add), so the low bits of the gradients vary from run to run (the forward is
+ * deterministic).  May be called more than once per forward.  Errors: TRIPS_ERR_STATE (last
+ * forward not saved, or ws differs), TRIPS_ERR_ARG (null buffer with n > 0), TRIPS_ERR_ALIGN,
+ * TRIPS_ERR_CUDA. */
+int trips_splat_backward(trips_plan* plan, void* ws, const float* grad_pyramid, float* grad_pos_size,
+                         float* grad_opacity, float* grad_desc, float* grad_camera, void* stream);
 
 /* ---- introspection ----------------------------------------------------------------- */
 
@@ -184,7 +198,8 @@ int trips_splat_backward(trips_plan* plan, void* ws, const float* grad_pyramid, 
 int trips_read_stats(const trips_plan* plan, const void* ws, trips_stats* out, void* stream);
 
 /* Synchronises `stream` and copies debug state of the last forward into the device buffer
- * dst (sizes in trips_export).  Errors: TRIPS_ERR_STATE (no forward), TRIPS_ERR_ARG. */
+ * dst (sizes in trips_export).  Errors: TRIPS_ERR_STATE (no saved forward; SCREEN_GRADS: no
+ * backward since the last trips_project), TRIPS_ERR_ARG, TRIPS_ERR_ALIGN. */
 int trips_debug_export(const trips_plan* plan, const void* ws, int32_t what, void* dst, void* stream);
 
 /* Per-stage device timing.  When enabled, CUDA events bracket every kernel stage
@@ -223,6 +238,25 @@ int trips_morton_order(void* ws, int64_t n, const float* pos, int32_t* perm_out,
  * Errors: TRIPS_ERR_ARG, TRIPS_ERR_ALIGN, TRIPS_ERR_CAPACITY (n >= 2^30), TRIPS_ERR_CUDA. */
 size_t trips_knn_workspace_bytes(int64_t n);
 int trips_knn_sizes(void* ws, int64_t n, const float* pos, float* size_out, int32_t* nbr_out, void* stream);
+
+/* ---- measurement ------------------------------------------------------------------ */
+
+/* Memory-operation microbenchmark giving the measured ceilings the backward's gradient
+ * reductions are reported against ("random-address red.add.f32 and atomicAdd
+ * u32 on L2-resident and DRAM-sized arrays").  Not part of the rasterizer path.
+ *   op        0 red.global.add.v4.f32, 1 red.global.add.f32, 2 atomicAdd u32 (result used),
+ *             3 st.global.v4 (scatter store), 4 ld.global.cg.v4 (gather load)
+ *   pattern   0: every lane an independent random row; 1: the 32 lanes of a warp hit 32
+ *             consecutive rows from a random base (spatially coherent, like a Morton cloud)
+ *   buf       device buffer of `bytes` bytes, 16-B aligned (contents are modified); the rows
+ *             used are the largest power of two of `row_bytes`-byte rows that fit in it
+ *   ops       requested operations (rounded up to whole iterations of 8 CTAs x 256 threads
+ *             per SM); *ops_done (nullable) receives the count issued
+ *   ms_out    device time of the one launch (CUDA events on `stream`); SYNCHRONISES `stream`.
+ * Errors: TRIPS_ERR_ARG (bad op/pattern, row_bytes not a multiple of 16, bytes < 64 rows),
+ * TRIPS_ERR_ALIGN, TRIPS_ERR_CUDA. */
+int trips_microbench(int32_t op, int32_t pattern, void* buf, int64_t bytes, int32_t row_bytes, int64_t ops,
+                     void* stream, double* ms_out, int64_t* ops_done);
 
 /* Total kernel launches issued by this library in this process. */
 int64_t trips_launch_count(void);

@@ -22,6 +22,7 @@ TRIPS_FWD_SAVE_FOR_BACKWARD = 1
 TRIPS_EXPORT_COUNTS = 1
 TRIPS_EXPORT_KEPT = 2
 TRIPS_EXPORT_KEPT_LAYER = 3
+TRIPS_EXPORT_SCREEN_GRADS = 4
 N_STAGES = 5
 STAGE_NAMES = ("count", "emit", "sort", "raster", "backward")
 
@@ -61,11 +62,10 @@ SIGNATURES = [
     ("trips_pyramid_floats", C.c_int64, [_VP]),
     ("trips_layer_dims", C.c_int, [_VP, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                    C.POINTER(C.c_int64)]),
-    ("trips_grad_stride", C.c_int32, [_VP]),
     ("trips_project", C.c_int, [_VP, _VP, C.POINTER(trips_camera), C.c_int64, _VP, _VP, _VP, _VP, _VP, _VP,
                                 _VP]),
     ("trips_splat_forward", C.c_int, [_VP, _VP, _VP, C.c_uint32, _VP]),
-    ("trips_splat_backward", C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP]),
+    ("trips_splat_backward", C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP]),
     ("trips_read_stats", C.c_int, [_VP, _VP, C.POINTER(trips_stats), _VP]),
     ("trips_debug_export", C.c_int, [_VP, _VP, C.c_int32, _VP, _VP]),
     ("trips_set_profiling", C.c_int, [_VP, C.c_int32]),
@@ -74,6 +74,8 @@ SIGNATURES = [
     ("trips_morton_order", C.c_int, [_VP, C.c_int64, _VP, _VP, _VP]),
     ("trips_knn_workspace_bytes", C.c_size_t, [C.c_int64]),
     ("trips_knn_sizes", C.c_int, [_VP, C.c_int64, _VP, _VP, _VP, _VP]),
+    ("trips_microbench", C.c_int, [C.c_int32, C.c_int32, _VP, C.c_int64, C.c_int32, C.c_int64, _VP,
+                                   C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
     ("trips_launch_count", C.c_int64, []),
     ("trips_status_string", C.c_char_p, [C.c_int]),
 ]
@@ -136,10 +138,6 @@ def trips_layer_dims(plan, l):
     return h.value, w.value, off.value
 
 
-def trips_grad_stride(plan):
-    return int(lib().trips_grad_stride(plan))
-
-
 def camera_struct(cam):
     """Any object with fx, fy, cx, cy, f, R (3x3), t (3), width, height, near."""
     c = trips_camera()
@@ -164,8 +162,10 @@ def trips_splat_forward(plan, ws, pyramid, flags, stream=None):
     return lib().trips_splat_forward(plan, ws, pyramid, flags, stream)
 
 
-def trips_splat_backward(plan, ws, grad_pyramid, grad, grad_camera=None, stream=None):
-    return lib().trips_splat_backward(plan, ws, grad_pyramid, grad, grad_camera, stream)
+def trips_splat_backward(plan, ws, grad_pyramid, grad_pos_size, grad_opacity, grad_desc, grad_camera=None,
+                         stream=None):
+    return lib().trips_splat_backward(plan, ws, grad_pyramid, grad_pos_size, grad_opacity, grad_desc, grad_camera,
+                                      stream)
 
 
 def trips_read_stats(plan, ws, stream=None):
@@ -203,6 +203,17 @@ def trips_knn_workspace_bytes(n):
 
 def trips_knn_sizes(ws, n, pos, size_out, nbr_out=None, stream=None):
     return lib().trips_knn_sizes(ws, n, pos, size_out, nbr_out, stream)
+
+
+MB_OPS = {"red_v4_f32": 0, "red_f32": 1, "atomic_add_u32": 2, "store_v4": 3, "load_v4": 4}
+
+
+def trips_microbench(op, pattern, buf, nbytes, row_bytes, ops, stream=None):
+    """Returns (ms, ops_done) of one microbenchmark launch (synchronises the stream)."""
+    ms, done = C.c_double(), C.c_int64()
+    check(lib().trips_microbench(op, pattern, buf, nbytes, row_bytes, ops, stream, C.byref(ms), C.byref(done)),
+          "trips_microbench")
+    return ms.value, done.value
 
 
 def trips_launch_count():

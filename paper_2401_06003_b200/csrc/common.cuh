@@ -64,8 +64,13 @@ struct Params {
     uint16_t* bin_orig;    // [8n]     footprint origin in the tile: (qx0+1) | (qy0+1) << 5
     uint32_t* pix_cnt;     // [T*256]  list length per tile pixel
     uint32_t* pix_meta;    // [T*256]  K (kept-list length; T_min: the cut length)
-    uint64_t* kept;        // [T*4096] kept (z, i) keys in blend order, [tile][m][pixel]; with
-                           //          coarse inclusion (z, i << 4 | d)
+    uint64_t* kept;        // [T*4096] coarse inclusion only: kept (z, i << 4 | d) keys in blend
+                           //          order, [tile][m][pixel]
+    uint64_t* kp_key;      // [T*4096] kept (point, tile) pairs of each tile, compact: (z, i) key
+    uint32_t* kp_info;     // [T*4096] footprint origin in the tile (bits 0-9, as bin_orig), kept
+                           //          corner mask (10-13), slot m of corner c in its pixel's kept
+                           //          list (bits 14 + 4c .. 17 + 4c)
+    uint32_t* kp_cnt;      // [T]      kept pairs per tile
     uint64_t* own;         // [T][16][256] coarse inclusion only: each pixel's own sorted top-16
     float* kept_gamma;     // [T*4096] gamma of each kept fragment (saved for the backward)
     unsigned long long* stats;  // [8]  n_culled, n_visible, n_pairs, n_frag, n_kept, n_trunc, max_list

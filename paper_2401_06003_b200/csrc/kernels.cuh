@@ -27,11 +27,26 @@ namespace trips {
 #ifndef TRIPS_THR_SKIP0
 #define TRIPS_THR_SKIP0 1
 #endif
+#ifndef TRIPS_BLEND_REG
+#define TRIPS_BLEND_REG 0
+#endif
+#ifndef TRIPS_PF_UNROLL
+#define TRIPS_PF_UNROLL 2
+#endif
+
+#ifndef TRIPS_RED_CLOBBER
+#define TRIPS_RED_CLOBBER 1
+#endif
 #ifndef TRIPS_BWD_CTAS
 #define TRIPS_BWD_CTAS 3
 #endif
 constexpr int kChunk = TRIPS_CHUNK;         // (point, tile) pairs staged per K4 iteration
 constexpr int kPairsPerThread = kChunk / kTilePix;
+constexpr int kPfUnroll = TRIPS_PF_UNROLL;      // bin pairs loaded together in k_raster phase F
+#ifndef TRIPS_BWD_SLOTS
+#define TRIPS_BWD_SLOTS 4
+#endif
+constexpr int kBwdSlots = TRIPS_BWD_SLOTS;      // kept pairs per thread held in registers across k_backward_pairs' phases
 #ifndef TRIPS_BWD_BATCH
 #define TRIPS_BWD_BATCH 4
 #endif
@@ -61,9 +76,14 @@ __device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float 
 {
 #ifdef TRIPS_EXP_NORED      // experiment builds only (tools/variants.sh): measure without the reductions
     if (a == 1.2345e-38f) *addr = b + c + d;
-#else
+#elif TRIPS_RED_CLOBBER
     asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};"
                  :: "l"(addr), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+#else
+    // no "memory" clobber: nothing in the kernel reads the gradient rows, so the compiler may
+    // move the next fragments' record loads above these reductions
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};"
+                 :: "l"(addr), "f"(a), "f"(b), "f"(c), "f"(d));
 #endif
 }
 
@@ -346,6 +366,15 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
         return;
     }
 
+#if !TRIPS_BLEND_REG
+    // The sorted top-16 moves to the (now free) chunk buffer, [m][pixel]: the blend reads its
+    // indices from there and phase F binary-searches it, so the 16 key registers die here.
+    __syncthreads();                                 // other lanes may still read s_keys (phase C)
+    uint64_t* s_kk = s_keys;                         // 16 x 256 keys (= kChunk * 4)
+#pragma unroll
+    for (int mm = 0; mm < kCap; ++mm) s_kk[mm * kTilePix + tid] = r[mm];   // kKeyMax beyond K
+#endif
+
     // phase D: front-to-back blend of the kept list (Eqs. 5-6; alpha_m := gamma_m, Q10).
     // Record gathers are issued kBatch at a time.  Without a following backward the loop
     // stops once T == 0 exactly (later terms vanish); with one, every gamma_m is needed.
@@ -366,8 +395,12 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
         float4 rb[kBlendBatch][1 + FC / 4];
 #pragma unroll
         for (int u = 0; u < kBlendBatch; ++u) {
-            const int mm = b * kBlendBatch + u;                  // compile-time register index
+            const int mm = b * kBlendBatch + u;
+#if TRIPS_BLEND_REG
             const uint32_t ii = (uint32_t)(mm < K ? r[mm] : r[0]);
+#else
+            const uint32_t ii = (uint32_t)s_kk[(mm < K ? mm : 0) * kTilePix + tid];
+#endif
             gather_record<FC>(P, ii, rb[u]);
         }
 #pragma unroll
@@ -401,16 +434,62 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
     }
     TRIPS_PCLK(5);
 
-    // phase E: store the sorted kept lists and per-pixel metadata
+    // phase E: per-pixel metadata
     P.pix_cnt[(size_t)t * kTilePix + tid] = valid ? total : 0u;
     P.pix_meta[(size_t)t * kTilePix + tid] = (uint32_t)Keff;
-    if (save) {
-        uint64_t* kp = P.kept + kidx;
-#pragma unroll
-        for (int mm = 0; mm < kCap; ++mm)
-            if (mm < Keff) kp[(size_t)mm * KS] = r[mm];
-    }
     TRIPS_PCLK(6);
+    if (!save) return;
+#ifdef TRIPS_EXP_NOPF
+    if (tid == 0) P.kp_cnt[t] = 0;
+    return;
+#endif
+
+    // phase F: the sorted kept lists stored as the tile's kept (point, tile)
+    // PAIRS: a pair of the bin is kept at corner c iff its key is among the first Keff keys of
+    // that corner's pixel; its slot m there is the key's rank (binary search of the pixel's
+    // sorted list, staged in shared memory).  A point's <= 4 kept fragments in this tile then
+    // travel together: the backward gathers its record and reduces its gradient once per pair
+    // instead of once per fragment (2.8x fewer scattered L2 operations at C4).
+#if TRIPS_BLEND_REG
+    __syncthreads();                                 // other lanes may still read s_keys (phase C)
+    uint64_t* s_kk = s_keys;                         // 16 x 256 keys (= kChunk * 4)
+#pragma unroll
+    for (int mm = 0; mm < kCap; ++mm) s_kk[mm * kTilePix + tid] = r[mm];   // kKeyMax beyond K
+#endif
+    // per-pixel kept threshold: the Keff-th key (a key of this pixel is kept iff <= it)
+    s_thr[tid] = Keff > 0 ? s_kk[(Keff - 1) * kTilePix + tid] : 0ull;
+    if (tid == 0) s_warp[0] = 0;
+    __syncthreads();
+    const size_t kpb = kept_base(t);
+    const unsigned long long* bk = reinterpret_cast<const unsigned long long*>(P.bin_key) + b0;
+    const uint16_t* bo = P.bin_orig + b0;
+    // classify one pair: kept corners and their slots; emit it if any corner is kept
+    auto pair_f = [&](bool in, uint64_t key, uint32_t o) {
+        const int q0 = (int)(o & 31u) - 1 + ((int)((o >> 5) & 31u) - 1) * kTile;
+        uint32_t info = o & 0x3ffu;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const int q = q0 + (c & 1) + (c >> 1) * kTile;
+            if (in && (o & (1u << (10 + c))) && key <= s_thr[q]) {
+                const uint64_t* L = s_kk + q;
+                int p = 0;
+                p += L[(p + 7) * kTilePix] < key ? 8 : 0;
+                p += L[(p + 3) * kTilePix] < key ? 4 : 0;
+                p += L[(p + 1) * kTilePix] < key ? 2 : 0;
+                p += L[p * kTilePix] < key ? 1 : 0;
+                info |= (1u << (10 + c)) | ((uint32_t)p << (14 + 4 * c));
+            }
+        }
+        if (info & 0x3c00u) {
+            const uint32_t slot = atomicAdd(&s_warp[0], 1u);
+            P.kp_key[kpb + slot] = key;
+            P.kp_info[kpb + slot] = info;
+        }
+    };
+    for (uint32_t j = tid; j < ((M + kTilePix - 1) & ~(uint32_t)(kTilePix - 1)); j += kTilePix)
+        pair_f(j < M, j < M ? __ldg(bk + j) : 0ull, j < M ? __ldg(bo + j) : 0u);
+    __syncthreads();
+    if (tid == 0) P.kp_cnt[t] = s_warp[0];
 }
 
 // --------------------------------------------------------------------------- K4c coarse blend
@@ -514,14 +593,44 @@ __global__ void __launch_bounds__(kTilePix) k_coarse_blend(Params P, float* __re
 
 // --------------------------------------------------------------------------- K5 backward
 
-// Screen-space gradient of one point (gxs, gys, gs: d/dx, d/dy, d/ds in image pixels; galpha;
-// gtau[F]) -> world space through the projection chain (Eq. 2, Sec. 3.1), reduced into its
-// packed row with 16-byte vector reductions; CAM: camera partials into cg.
-template <int FC, bool CAM>
+// Caller's gradient buffers (trips_splat_backward): pos_size [n] float4 (dL/dx, dL/dy, dL/dz,
+// dL/ds_w), opacity [n], desc [n][F] (vector reductions when the rows allow it: desc_vec = 4 for
+// F % 4 == 0 and 16-B aligned rows, 2 for F % 2 == 0 and 8-B aligned, else 1).  `screen`
+// (debug export only) receives the screen-space gradients [n][4 + F] instead.
+struct GradOut {
+    float* pos_size;
+    float* opacity;
+    float* desc;
+    float* screen;
+    int desc_vec;
+};
+
+__device__ __forceinline__ void red_add_v2(float* addr, float a, float b)
+{
+    asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" :: "l"(addr), "f"(a), "f"(b));
+}
+__device__ __forceinline__ void red_add_f32(float* addr, float a)
+{
+    asm volatile("red.global.add.f32 [%0], %1;" :: "l"(addr), "f"(a));
+}
+
+// Screen-space gradient of one point in one view (gxs, gys, gs: d/dx, d/dy, d/ds in layer-0
+// pixels; galpha; gtau[F]) -> world space through the projection chain (Eq. 2, Sec. 3.1), added
+// to the caller's buffers with vector reductions; CAM: camera partials into cg.  SCREEN (debug
+// export): the screen-space values are added to go.screen instead.
+template <int FC, bool CAM, bool SCREEN>
 __device__ __forceinline__ void point_reduce(const Params& P, uint32_t i, float4 r0, float z, float gxs, float gys,
-                                             float gs, float galpha, const float (&gtau)[FC], float* __restrict__ grad,
+                                             float gs, float galpha, const float (&gtau)[FC], const GradOut& go,
                                              float (&cg)[CAM ? 17 : 1])
 {
+    if (SCREEN) {
+        float* d = go.screen + (size_t)i * (4 + P.F);
+        atomicAdd(d + 0, gxs); atomicAdd(d + 1, gys); atomicAdd(d + 2, gs); atomicAdd(d + 3, galpha);
+#pragma unroll
+        for (int c = 0; c < FC; ++c)
+            if (c < P.F) atomicAdd(d + 4 + c, gtau[c]);
+        return;
+    }
     const Cam& cam = P.cam;
     const float iz = 1.0f / z;
     const float gpx = gxs * cam.fx * iz, gpy = gys * cam.fy * iz;
@@ -550,21 +659,234 @@ __device__ __forceinline__ void point_reduce(const Params& P, uint32_t i, float4
         cg[15] += gys;
         cg[16] = fmaf(gs, r0.z / cam.f, cg[16]);
     }
-    float* grow = grad + (size_t)i * P.G;
-    red_add_v4(grow, gX, gY, gZ, gsw);
-    float v[FC + 4];
-    v[0] = galpha;
+    red_add_v4(go.pos_size + (size_t)i * 4, gX, gY, gZ, gsw);
+    red_add_f32(go.opacity + i, galpha);
+    float* dr = go.desc + (size_t)i * P.F;
+    if (go.desc_vec == 4) {
 #pragma unroll
-    for (int c = 0; c < FC; ++c) v[1 + c] = gtau[c];
-    v[FC + 1] = 0.f; v[FC + 2] = 0.f; v[FC + 3] = 0.f;
+        for (int c4 = 0; c4 < FC / 4; ++c4) red_add_v4(dr + 4 * c4, gtau[4 * c4], gtau[4 * c4 + 1], gtau[4 * c4 + 2], gtau[4 * c4 + 3]);
+    } else if (go.desc_vec == 2) {
 #pragma unroll
-    for (int c4 = 0; c4 < (FC + 4) / 4; ++c4)
-        if (4 * c4 < P.F + 1) red_add_v4(grow + 4 + 4 * c4, v[4 * c4], v[4 * c4 + 1], v[4 * c4 + 2], v[4 * c4 + 3]);
+        for (int c2 = 0; c2 < FC / 2; ++c2)
+            if (2 * c2 < P.F) red_add_v2(dr + 2 * c2, gtau[2 * c2], gtau[2 * c2 + 1]);
+    } else {
+#pragma unroll
+        for (int c = 0; c < FC; ++c)
+            if (c < P.F) red_add_f32(dr + c, gtau[c]);
+    }
 }
 
-template <int FC, bool CAM, bool COARSE>
-__global__ void __launch_bounds__(kTilePix, FC <= 4 ? TRIPS_BWD_CTAS : 2) k_backward(Params P, const float* __restrict__ gpyr,
-                                                       float* __restrict__ grad, float* __restrict__ grad_cam)
+// Block reduction of the 17 camera-gradient partials, 17 atomics per tile (all threads call).
+__device__ __forceinline__ void camera_block_reduce(float (&cg)[17], float* grad_cam)
+{
+    __shared__ float s_cg[kTilePix / 32][17];
+    const int tid = threadIdx.x;
+#pragma unroll
+    for (int k = 0; k < 17; ++k) {
+        float v = cg[k];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if ((tid & 31) == 0) s_cg[tid >> 5][k] = v;
+    }
+    __syncthreads();
+    if (tid < 17) {
+        float v = 0.f;
+#pragma unroll
+        for (int w = 0; w < kTilePix / 32; ++w) v += s_cg[w][tid];
+        if (v != 0.f) atomicAdd(grad_cam + tid, v);
+    }
+}
+
+// Pair-wise backward (non-coarse): one CTA per tile, three phases over the tile's kept pairs
+// (written by k_raster phase F) and its pixels.
+//   P1 per kept pair: gather tau_i once; for each kept corner (pixel q, slot m) c = <gC_q, tau_i>
+//   P2 per pixel: T_m from the saved gamma_m (Eq. 6) and the reverse suffix recurrence
+//      dL/dgamma_m = T_m (c_m - S_m + gA (1 - b_m)),  S_{m-1} = gamma_m c_m + (1 - gamma_m) S_m,
+//      b_{m-1} = gamma_m + (1 - gamma_m) b_m  (division-free)
+//   P3 per kept pair: gather the screen record once, sum the chain of Eq. (3)-(4) over its kept
+//      corners (beta = wx wy, iota(s)) and dL/dtau = sum T_m gamma_m gC_q, then ONE world-space
+//      reduction set per pair (point_reduce).
+template <int FC, bool CAM, bool SCREEN>
+__global__ void __launch_bounds__(kTilePix, TRIPS_BWD_CTAS) k_backward_pairs(Params P, const float* __restrict__ gpyr,
+                                                                             GradOut go, float* __restrict__ grad_cam)
+{
+    // [channel][pixel] upstream gradient of the tile (static shared memory stays <= 48 KB up to
+    // FC = 12; wider descriptors read it from the pyramid through L1 instead)
+    constexpr bool kGs = FC <= 12;
+    __shared__ float s_g[kGs ? FC * kTilePix : 1];
+    __shared__ float s_c[kCap * kTilePix];           // [m][pixel] c_m, then dL/dgamma_m
+    __shared__ float s_tg[kCap * kTilePix];          // [m][pixel] T_m gamma_m
+    const int t = blockIdx.x;
+    const uint32_t npair = P.kp_cnt[t];
+    if (npair == 0) return;                          // uniform: nothing kept in this tile
+    const TileCoord tc = tile_coord(P, t);
+    const LayerGeom& G = P.L[tc.l];
+    const int tid = threadIdx.x;
+    const int x_lo = tc.tx * kTile, y_lo = tc.ty * kTile;
+    const int px = x_lo + (tid & (kTile - 1)), py = y_lo + (tid >> 4);
+    const int K = (int)(P.pix_meta[(size_t)t * kTilePix + tid] & 31u);
+    const int64_t plane = (int64_t)G.W * G.H;
+    const float* gtile = gpyr + G.float_off + (int64_t)y_lo * G.W + x_lo;   // pixel q at (q & 15) + (q >> 4) W
+    auto gC = [&](int f, int q) -> float {
+        if constexpr (kGs) return s_g[f * kTilePix + q];
+        else return f < P.F ? __ldg(gtile + f * plane + (int64_t)(q >> 4) * G.W + (q & (kTile - 1))) : 0.f;
+    };
+    float gA = 0.f;
+    if (K > 0) {
+        const float* gp = gpyr + G.float_off + (int64_t)py * G.W + px;
+        if constexpr (kGs) {
+#pragma unroll
+            for (int c = 0; c < FC; ++c) s_g[c * kTilePix + tid] = c < P.F ? __ldg(gp + c * plane) : 0.f;
+        }
+        gA = __ldg(gp + P.F * plane);
+    }
+    __syncthreads();
+    const size_t kpb = kept_base(t);
+    const unsigned long long* kkey = reinterpret_cast<const unsigned long long*>(P.kp_key) + kpb;
+    const uint32_t* kinfo = P.kp_info + kpb;
+
+    // P1: c = <gC_q, tau_i> for every kept corner.  The first kBwdSlots pairs of each thread keep
+    // their key, info and screen record in registers for P3 (all their loads are issued before
+    // the first use); pairs beyond kBwdSlots * 256 (dense tiles) are re-read in P3.
+    auto corners_c = [&](uint32_t info, const float4 (&tb)[FC / 4]) {
+        const int q0 = (int)(info & 31u) - 1 + ((int)((info >> 5) & 31u) - 1) * kTile;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            if (info & (1u << (10 + c))) {
+                const int q = q0 + (c & 1) + (c >> 1) * kTile;
+                const int m = (int)((info >> (14 + 4 * c)) & 15u);
+                float d = 0.f;
+#pragma unroll
+                for (int c4 = 0; c4 < FC / 4; ++c4) {
+                    d = fmaf(gC(4 * c4 + 0, q), tb[c4].x, d);
+                    d = fmaf(gC(4 * c4 + 1, q), tb[c4].y, d);
+                    d = fmaf(gC(4 * c4 + 2, q), tb[c4].z, d);
+                    d = fmaf(gC(4 * c4 + 3, q), tb[c4].w, d);
+                }
+                s_c[m * kTilePix + q] = d;
+            }
+        }
+    };
+    uint64_t rkey[kBwdSlots];
+    uint32_t rinfo[kBwdSlots];
+    float4 rgeo[kBwdSlots];
+    {
+        float4 rtau[kBwdSlots][FC / 4];
+#pragma unroll
+        for (int u = 0; u < kBwdSlots; ++u) {
+            const uint32_t j = tid + u * kTilePix;
+            rkey[u] = j < npair ? __ldg(kkey + j) : 0ull;
+            rinfo[u] = j < npair ? __ldg(kinfo + j) : 0u;            // no corner bits: inert
+        }
+#pragma unroll
+        for (int u = 0; u < kBwdSlots; ++u) {
+            const uint32_t i = (uint32_t)rkey[u];
+            if (rinfo[u]) {
+                const float4* tp = reinterpret_cast<const float4*>(P.tau + (size_t)i * FC);
+#pragma unroll
+                for (int c4 = 0; c4 < FC / 4; ++c4) rtau[u][c4] = __ldg(tp + c4);
+                rgeo[u] = __ldg(P.geo + i);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kBwdSlots; ++u)
+            if (rinfo[u]) corners_c(rinfo[u], rtau[u]);
+    }
+    for (uint32_t j = tid + kBwdSlots * kTilePix; j < npair; j += kTilePix) {
+        const uint32_t i = (uint32_t)__ldg(kkey + j);
+        const uint32_t info = __ldg(kinfo + j);
+        float4 tb[FC / 4];
+        const float4* tp = reinterpret_cast<const float4*>(P.tau + (size_t)i * FC);
+#pragma unroll
+        for (int c4 = 0; c4 < FC / 4; ++c4) tb[c4] = __ldg(tp + c4);
+        corners_c(info, tb);
+    }
+    __syncthreads();
+
+    // P2: per pixel, T_m and the reverse suffix recurrence
+    if (K > 0) {
+        const float* gm = P.kept_gamma + kpb + tid;
+        float gam[kCap];
+#pragma unroll
+        for (int mm = 0; mm < kCap; ++mm) gam[mm] = mm < K ? __ldg(gm + mm * kTilePix) : 0.f;
+        float Tm[kCap];
+        float T = 1.f;
+#pragma unroll
+        for (int mm = 0; mm < kCap; ++mm) { Tm[mm] = T; T = T * (1.0f - gam[mm]); }
+        float S = 0.f, bb = 0.f;
+#pragma unroll
+        for (int mm = kCap - 1; mm >= 0; --mm) {
+            if (mm < K) {
+                const float g = gam[mm];
+                const float c = s_c[mm * kTilePix + tid];
+                s_c[mm * kTilePix + tid] = Tm[mm] * (c - S + gA * (1.0f - bb));
+                s_tg[mm * kTilePix + tid] = Tm[mm] * g;
+                S = g * c + (1.0f - g) * S;
+                bb = g + (1.0f - g) * bb;
+            }
+        }
+    }
+    __syncthreads();
+
+    // P3: per kept pair, the chain summed over its kept corners, one reduction set
+    float cg[CAM ? 17 : 1];
+#pragma unroll
+    for (int k = 0; k < (CAM ? 17 : 1); ++k) cg[k] = 0.f;
+    const float sc = pow2_neg(tc.l);
+    auto pair_chain = [&](uint64_t key, uint32_t info, float4 r0) {
+        const uint32_t i = (uint32_t)key;
+        const float z = __uint_as_float((uint32_t)(key >> 32));
+        const Levels lv = select_levels(r0.z, P.n_layers);
+        const bool upper = tc.l != lv.lo;                // this tile's layer is the point's second one
+        const float iota = upper ? lv.iota[1] : lv.iota[0];
+        const float diota = upper ? lv.diota[1] : lv.diota[0];
+        const float xl = __fmul_rn(r0.x, sc), yl = __fmul_rn(r0.y, sc);
+        const float fx = __fsub_rn(xl, floorf(xl)), fy = __fsub_rn(yl, floorf(yl));
+        const int q0 = (int)(info & 31u) - 1 + ((int)((info >> 5) & 31u) - 1) * kTile;
+        float gbx = 0.f, gby = 0.f, gal = 0.f;
+        float gt[FC];
+#pragma unroll
+        for (int c = 0; c < FC; ++c) gt[c] = 0.f;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            if (info & (1u << (10 + c))) {
+                const int q = q0 + (c & 1) + (c >> 1) * kTile;
+                const int m = (int)((info >> (14 + 4 * c)) & 15u);
+                const float dg = s_c[m * kTilePix + q];
+                const float tg = s_tg[m * kTilePix + q];
+                const float wx = (c & 1) ? fx : __fsub_rn(1.0f, fx);
+                const float wy = (c & 2) ? fy : __fsub_rn(1.0f, fy);
+                const float beta = wx * wy;
+                gal = fmaf(dg, beta, gal);                   // * iota at the end
+                // d beta / d x_l = wy * (dx ? +1 : -1), d beta / d y_l = wx * (dy ? +1 : -1)
+                gbx = fmaf(dg, (c & 1) ? wy : -wy, gbx);     // * iota alpha 2^-l
+                gby = fmaf(dg, (c & 2) ? wx : -wx, gby);
+#pragma unroll
+                for (int f = 0; f < FC; ++f) gt[f] = fmaf(tg, gC(f, q), gt[f]);
+            }
+        }
+        const float ia = iota * r0.w;
+        const float gxs = gbx * ia * sc, gys = gby * ia * sc;
+        const float gs = gal * r0.w * diota;             // d gamma / d iota = beta alpha
+        const float galpha = gal * iota;                 // d gamma / d alpha = beta iota
+        point_reduce<FC, CAM, SCREEN>(P, i, r0, z, gxs, gys, gs, galpha, gt, go, cg);
+    };
+#pragma unroll
+    for (int u = 0; u < kBwdSlots; ++u)
+        if (rinfo[u]) pair_chain(rkey[u], rinfo[u], rgeo[u]);
+    for (uint32_t j = tid + kBwdSlots * kTilePix; j < npair; j += kTilePix) {
+        const uint64_t key = __ldg(kkey + j);
+        pair_chain(key, __ldg(kinfo + j), __ldg(P.geo + (uint32_t)key));
+    }
+    if constexpr (CAM) camera_block_reduce(cg, grad_cam);
+}
+
+// Per-pixel backward over the kept (z, i << 4 | d) lists of coarse-layer inclusion (reading Q22):
+// the blended fragments of a pixel come from several layers and tiles, so they are replayed per
+// pixel and reduced per fragment.
+template <int FC, bool CAM, bool SCREEN>
+__global__ void __launch_bounds__(kTilePix, FC <= 4 ? TRIPS_BWD_CTAS : 2) k_backward_coarse(Params P, const float* __restrict__ gpyr,
+                                                       GradOut go, float* __restrict__ grad_cam)
 {
     const int t = blockIdx.x;
     const TileCoord tc = tile_coord(P, t);
@@ -606,7 +928,6 @@ __global__ void __launch_bounds__(kTilePix, FC <= 4 ? TRIPS_BWD_CTAS : 2) k_back
 #pragma unroll
     for (int c = 0; c < FC; ++c) B[c] = 0.f;
     float bb = 0.f;
-    const float sc0 = pow2_neg(tc.l);
 #pragma unroll
     for (int b = kCap / kBatch - 1; b >= 0; --b) {
         if (b * kBatch >= K) continue;
@@ -616,16 +937,16 @@ __global__ void __launch_bounds__(kTilePix, FC <= 4 ? TRIPS_BWD_CTAS : 2) k_back
         for (int u = 0; u < kBatch; ++u) {
             const int mm = min(b * kBatch + u, K - 1);
             kb[u] = __ldg(reinterpret_cast<const unsigned long long*>(kp) + mm * KS);
-            const uint32_t iu = COARSE ? (uint32_t)kb[u] >> 4 : (uint32_t)kb[u];
+            const uint32_t iu = (uint32_t)kb[u] >> 4;
             gather_record<FC>(P, iu, rb[u]);
         }
 #pragma unroll
         for (int u = kBatch - 1; u >= 0; --u) {
             const int mm = b * kBatch + u;
             if (mm >= K) continue;
-            const uint32_t i = COARSE ? (uint32_t)kb[u] >> 4 : (uint32_t)kb[u];
-            const int d = COARSE ? (int)(kb[u] & 15u) : 0;
-            const float sc = COARSE ? pow2_neg(tc.l + d) : sc0;
+            const uint32_t i = (uint32_t)kb[u] >> 4;
+            const int d = (int)(kb[u] & 15u);
+            const float sc = pow2_neg(tc.l + d);
             const float z = __uint_as_float((uint32_t)(kb[u] >> 32));
             const float4 r0 = rb[u][0];
             const FragW w = frag_weights(r0, tc.l + d, P.n_layers, px >> d, py >> d);
@@ -650,30 +971,13 @@ __global__ void __launch_bounds__(kTilePix, FC <= 4 ? TRIPS_BWD_CTAS : 2) k_back
             float gt[FC];
 #pragma unroll
             for (int c = 0; c < FC; ++c) gt[c] = tg * gC[c];
-            point_reduce<FC, CAM>(P, i, r0, z, gxs, gys, gs, galpha, gt, grad, cg);
+            point_reduce<FC, CAM, SCREEN>(P, i, r0, z, gxs, gys, gs, galpha, gt, go, cg);
 #pragma unroll
             for (int c = 0; c < FC; ++c) B[c] = g * tau[c] + (1.0f - g) * B[c];
             bb = g + (1.0f - g) * bb;
         }
     }
-    if (CAM) {
-        // block reduction of the 17 camera-gradient partials, 17 atomics per tile
-        __shared__ float s_cg[kTilePix / 32][17];
-#pragma unroll
-        for (int k = 0; k < 17; ++k) {
-            float v = cg[k];
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-            if ((tid & 31) == 0) s_cg[tid >> 5][k] = v;
-        }
-        __syncthreads();
-        if (tid < 17) {
-            float v = 0.f;
-#pragma unroll
-            for (int w = 0; w < kTilePix / 32; ++w) v += s_cg[w][tid];
-            if (v != 0.f) atomicAdd(grad_cam + tid, v);
-        }
-    }
+    if constexpr (CAM) camera_block_reduce(cg, grad_cam);
 }
 
 // --------------------------------------------------------------------------- export
@@ -685,19 +989,38 @@ __global__ void __launch_bounds__(kTilePix) k_export(Params P, int what, void* d
     const LayerGeom& G = P.L[tc.l];
     const int tid = threadIdx.x;
     const int px = tc.tx * kTile + (tid & (kTile - 1)), py = tc.ty * kTile + (tid >> 4);
-    if (px >= G.W || py >= G.H) return;
+    const bool valid = px < G.W && py < G.H;
     const int64_t pidx = G.pix_off + (int64_t)py * G.W + px;
     if (what == 1) {
-        static_cast<uint32_t*>(dst)[pidx] = P.pix_cnt[(size_t)t * kTilePix + tid];
-    } else {
+        if (valid) static_cast<uint32_t*>(dst)[pidx] = P.pix_cnt[(size_t)t * kTilePix + tid];
+        return;
+    }
+    int32_t* o = static_cast<int32_t*>(dst);
+    if (P.coarse) {
+        if (!valid) return;
         const uint32_t meta = P.pix_meta[(size_t)t * kTilePix + tid];
         const int K = (int)(meta & 31u);
         const uint64_t* kp = P.kept + kept_base(t) + tid;
-        int32_t* o = static_cast<int32_t*>(dst) + pidx * kCap;
         for (int m = 0; m < kCap; ++m) {
             const uint32_t lo = (uint32_t)kp[m * kTilePix];
-            if (what == 3) o[m] = m < K ? (P.coarse ? (int32_t)(lo & 15u) : 0) : -1;
-            else o[m] = m < K ? (int32_t)(P.coarse ? lo >> 4 : lo) : -1;
+            o[pidx * kCap + m] = m < K ? (what == 3 ? (int32_t)(lo & 15u) : (int32_t)(lo >> 4)) : -1;
+        }
+        return;
+    }
+    // plain / T_min: the kept lists are stored as kept (point, tile) pairs (k_raster phase F)
+    if (valid)
+        for (int m = 0; m < kCap; ++m) o[pidx * kCap + m] = -1;
+    __syncthreads();
+    const uint32_t npair = P.kp_cnt[t];
+    for (uint32_t j = tid; j < npair; j += kTilePix) {
+        const uint32_t i = (uint32_t)P.kp_key[kept_base(t) + j];
+        const uint32_t info = P.kp_info[kept_base(t) + j];
+        const int qx0 = (int)(info & 31u) - 1, qy0 = (int)((info >> 5) & 31u) - 1;
+        for (int c = 0; c < 4; ++c) {
+            if (!(info & (1u << (10 + c)))) continue;
+            const int m = (int)((info >> (14 + 4 * c)) & 15u);
+            const int64_t q = G.pix_off + (int64_t)(tc.ty * kTile + qy0 + (c >> 1)) * G.W + (tc.tx * kTile + qx0 + (c & 1));
+            o[q * kCap + m] = what == 3 ? 0 : (int32_t)i;
         }
     }
 }

@@ -7,12 +7,14 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "../../include/trips.h"
 #include "kernels.cuh"
 #include "knn.cuh"
 #include "morton.cuh"
+#include "microbench.cuh"
 
 using namespace trips;
 
@@ -41,13 +43,14 @@ struct trips_plan {
     // workspace layout (byte offsets)
     int32_t ctas;           // binning CTAs (persistent grid)
     size_t off_geo, off_tau, off_z, off_hist, off_cvis, off_toff, off_bkey, off_borig, off_pcnt, off_pmeta, off_kept, off_kgam,
-        off_own, off_stats, ws_bytes;
+        off_own, off_kpkey, off_kpinfo, off_kpcnt, off_stats, ws_bytes;
     // state
     const void* ws_bound = nullptr;
     int stage = 0;          // 0 none, 1 projected, 2 forward (saved), 3 forward (not saved)
     int64_t n = 0;
     Cam cam;
     const float* desc = nullptr;   // caller's descriptors of the last trips_project
+    const float* last_gpyr = nullptr;  // grad_pyramid of the last backward (SCREEN_GRADS export)
     bool tau_direct = false;       // gathered in place (F % 4 == 0, 16-B aligned)
     // profiling
     bool prof = false;
@@ -101,17 +104,34 @@ int cuda_status(cudaError_t e)
     return TRIPS_ERR_CUDA;
 }
 
+// Per-device host caches (SM count, shared-memory opt-ins), guarded by one mutex: a process may
+// drive several GPUs, and cudaFuncSetAttribute applies to the current device only.
+constexpr int kMaxDevices = 64;
+std::mutex g_dev_mu;
+
+int current_device()
+{
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) {
+        cudaGetLastError();
+        dev = 0;
+    }
+    return dev;
+}
+
 int num_sms()
 {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        if (cudaGetDevice(&dev) != cudaSuccess ||
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0)
-            sms = 148;                        // B200; plan creation must work without a GPU
+    static int sms[kMaxDevices] = {};
+    const int dev = current_device();
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    if (!sms[dev]) {
+        int v = 0;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0)
+            v = 148;                          // B200; plan creation must work without a GPU
         cudaGetLastError();
+        sms[dev] = v;
     }
-    return sms;
+    return sms[dev];
 }
 
 template <int FC>
@@ -123,7 +143,10 @@ int set_emit_attr(size_t bytes)
 // Opt the binning kernels into > 48 KB of dynamic shared memory (one counter per tile).
 int set_smem_attrs(size_t bytes)
 {
-    static size_t done = 0;
+    static size_t done_dev[kMaxDevices] = {};
+    const int dev = current_device();
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    size_t& done = done_dev[dev];
     if (bytes <= done) return TRIPS_OK;
     cudaError_t e = cudaFuncSetAttribute(k_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     int bad = (int)e;
@@ -146,7 +169,7 @@ Params make_params(const trips_plan* p, void* ws)
     Params P;
     memset(&P, 0, sizeof(P));
     P.n = (int32_t)p->n;
-    P.F = p->F; P.FC = p->FC; P.G = p->G;
+    P.F = p->F; P.FC = p->FC; P.G = 0;
     P.n_layers = p->n_layers; P.T = p->T;
     P.t_min = p->t_min;
     P.coarse = p->coarse;
@@ -165,7 +188,10 @@ Params make_params(const trips_plan* p, void* ws)
     P.bin_orig = reinterpret_cast<uint16_t*>(b + p->off_borig);
     P.pix_cnt = reinterpret_cast<uint32_t*>(b + p->off_pcnt);
     P.pix_meta = reinterpret_cast<uint32_t*>(b + p->off_pmeta);
-    P.kept = reinterpret_cast<uint64_t*>(b + p->off_kept);
+    P.kept = p->coarse ? reinterpret_cast<uint64_t*>(b + p->off_kept) : nullptr;
+    P.kp_key = p->coarse ? nullptr : reinterpret_cast<uint64_t*>(b + p->off_kpkey);
+    P.kp_info = p->coarse ? nullptr : reinterpret_cast<uint32_t*>(b + p->off_kpinfo);
+    P.kp_cnt = p->coarse ? nullptr : reinterpret_cast<uint32_t*>(b + p->off_kpcnt);
     P.kept_gamma = reinterpret_cast<float*>(b + p->off_kgam);
     P.own = p->coarse ? reinterpret_cast<uint64_t*>(b + p->off_own) : nullptr;
     P.stats = reinterpret_cast<unsigned long long*>(b + p->off_stats);
@@ -203,7 +229,7 @@ int trips_plan_create(const trips_config* cfg, int32_t width, int32_t height, in
     if (width < 1 || height < 1 || width > 32768 || height > 32768) return TRIPS_ERR_ARG;
     if (max_points < 0 || max_points >= (int64_t(1) << 28)) return TRIPS_ERR_ARG;
     trips_plan* p = new trips_plan();
-    p->n_layers = n; p->F = F; p->FC = (F + 3) & ~3; p->G = 8 + p->FC;
+    p->n_layers = n; p->F = F; p->FC = (F + 3) & ~3; p->G = 0;
     p->t_min = cfg->t_min;
     p->coarse = std::min(cfg->coarse_layers, n - 1);
     p->W = width; p->H = height; p->max_points = max_points;
@@ -240,7 +266,12 @@ int trips_plan_create(const trips_config* cfg, int32_t width, int32_t height, in
     p->off_borig = o;  o = align256(o + 8 * N * 2);
     p->off_pcnt = o;  o = align256(o + (size_t)tiles * kTilePix * 4);
     p->off_pmeta = o; o = align256(o + (size_t)tiles * kTilePix * 4);
-    p->off_kept = o;  o = align256(o + (p->kcap ? p->kcap : 1) * 8);
+    // kept lists: coarse inclusion keeps per-pixel key lists; otherwise the raster stores the
+    // tile's kept (point, tile) pairs (<= 4096 per tile) for the pair-wise backward
+    p->off_kept = o;  o = align256(o + (p->coarse ? p->kcap * 8 : 0));
+    p->off_kpkey = o; o = align256(o + (p->coarse ? 0 : p->kcap * 8));
+    p->off_kpinfo = o; o = align256(o + (p->coarse ? 0 : p->kcap * 4));
+    p->off_kpcnt = o; o = align256(o + (p->coarse ? 0 : (size_t)tiles * 4));
     p->off_kgam = o;  o = align256(o + (p->kcap ? p->kcap : 1) * 4);
     p->off_own = o;   o = align256(o + (p->coarse ? (size_t)tiles * kTilePix * kCap * 8 : 0));
     p->off_stats = o; o = align256(o + S_COUNT * 8);
@@ -261,7 +292,6 @@ void trips_plan_destroy(trips_plan* p)
 size_t trips_workspace_bytes(const trips_plan* p) { return p ? p->ws_bytes : 0; }
 int64_t trips_num_pixels(const trips_plan* p) { return p ? p->P : -1; }
 int64_t trips_pyramid_floats(const trips_plan* p) { return p ? p->pyr_floats : -1; }
-int32_t trips_grad_stride(const trips_plan* p) { return p ? p->G : -1; }
 
 int trips_layer_dims(const trips_plan* p, int32_t l, int32_t* h, int32_t* w, int64_t* off)
 {
@@ -290,6 +320,7 @@ int trips_project(trips_plan* p, void* ws, const trips_camera* c, int64_t n, con
     p->ws_bound = ws;
     p->stage = 0;
     p->n = n;
+    p->last_gpyr = nullptr;
     // descriptors are gathered straight from the caller's rows when they are whole float4s;
     // otherwise k_count writes a padded copy into the workspace
     p->desc = desc;
@@ -335,8 +366,11 @@ int trips_splat_forward(trips_plan* p, void* ws, float* pyramid, uint32_t flags,
         StageScope sc(p, 3, st);
         const int save = (flags & TRIPS_FWD_SAVE_FOR_BACKWARD) ? 1 : 0;
         const size_t rsm = (size_t)raster_dyn_smem();
-        static bool rattr[3][9] = {};
+        static bool rattr_dev[kMaxDevices][3][9] = {};
         const int mode = p->coarse ? kRasterOwn : (p->t_min > 0.f ? kRasterTmin : kRasterPlain);
+        const int dev = current_device();
+        std::lock_guard<std::mutex> lk(g_dev_mu);
+        bool (&rattr)[3][9] = rattr_dev[dev];
         if (!rattr[mode][p->FC / 4]) {
             const int a = (int)cudaFuncAttributeMaxDynamicSharedMemorySize;
             if (mode == kRasterOwn) {
@@ -363,33 +397,49 @@ int trips_splat_forward(trips_plan* p, void* ws, float* pyramid, uint32_t flags,
     return TRIPS_OK;
 }
 
-int trips_splat_backward(trips_plan* p, void* ws, const float* grad_pyramid, float* grad, float* grad_camera,
-                         void* stream)
+namespace {
+
+// Launches the backward of the last saved forward into the caller's buffers (go), or the
+// screen-space gradients into go.screen (SCREEN, debug export).
+int launch_backward(const trips_plan* p, const Params& P, const float* gpyr, const GradOut& go, float* gcam, bool screen,
+                    cudaStream_t st)
 {
-    if (!p || !ws || !grad_pyramid || !grad) return TRIPS_ERR_ARG;
+#define TRIPS_BWD(KERNEL, CAM, SCR) TRIPS_FC_SWITCH(p->FC, (KERNEL<kFC, CAM, SCR><<<p->T, kTilePix, 0, st>>>(P, gpyr, go, gcam)))
+    if (p->coarse) {
+        if (screen) { TRIPS_BWD(k_backward_coarse, false, true); }
+        else if (gcam) { TRIPS_BWD(k_backward_coarse, true, false); }
+        else { TRIPS_BWD(k_backward_coarse, false, false); }
+    } else {
+        if (screen) { TRIPS_BWD(k_backward_pairs, false, true); }
+        else if (gcam) { TRIPS_BWD(k_backward_pairs, true, false); }
+        else { TRIPS_BWD(k_backward_pairs, false, false); }
+    }
+#undef TRIPS_BWD
+    return check_launch();
+}
+
+}  // namespace
+
+int trips_splat_backward(trips_plan* p, void* ws, const float* grad_pyramid, float* grad_pos_size, float* grad_opacity,
+                         float* grad_desc, float* grad_camera, void* stream)
+{
+    if (!p || !ws || !grad_pyramid) return TRIPS_ERR_ARG;
+    if (p->n > 0 && (!grad_pos_size || !grad_opacity || !grad_desc)) return TRIPS_ERR_ARG;
     if (p->stage != 2 || ws != p->ws_bound) return TRIPS_ERR_STATE;
-    if (!aligned(grad_pyramid, 16) || !aligned(grad, 16) || !aligned(grad_camera, 4)) return TRIPS_ERR_ALIGN;
+    if (!aligned(grad_pyramid, 16) || !aligned(grad_pos_size, 16) || !aligned(grad_opacity, 4) ||
+        !aligned(grad_desc, 4) || !aligned(grad_camera, 4))
+        return TRIPS_ERR_ALIGN;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     Params P = make_params(p, ws);
-    int rc;
-    {
-        StageScope sc(p, 4, st);
-        if (grad_camera && p->coarse) {
-            TRIPS_FC_SWITCH(p->FC, (k_backward<kFC, true, true><<<p->T, kTilePix, 0, st>>>(P, grad_pyramid, grad,
-                                                                                             grad_camera)));
-        } else if (grad_camera) {
-            TRIPS_FC_SWITCH(p->FC, (k_backward<kFC, true, false><<<p->T, kTilePix, 0, st>>>(P, grad_pyramid, grad,
-                                                                                              grad_camera)));
-        } else if (p->coarse) {
-            TRIPS_FC_SWITCH(p->FC, (k_backward<kFC, false, true><<<p->T, kTilePix, 0, st>>>(P, grad_pyramid, grad,
-                                                                                              nullptr)));
-        } else {
-            TRIPS_FC_SWITCH(p->FC, (k_backward<kFC, false, false><<<p->T, kTilePix, 0, st>>>(P, grad_pyramid, grad,
-                                                                                               nullptr)));
-        }
-        if ((rc = check_launch())) return rc;
-    }
-    return TRIPS_OK;
+    GradOut go;
+    go.pos_size = grad_pos_size;
+    go.opacity = grad_opacity;
+    go.desc = grad_desc;
+    go.screen = nullptr;
+    go.desc_vec = (p->F % 4 == 0 && aligned(grad_desc, 16)) ? 4 : ((p->F % 2 == 0 && aligned(grad_desc, 8)) ? 2 : 1);
+    p->last_gpyr = grad_pyramid;
+    StageScope sc(p, 4, st);
+    return launch_backward(p, P, grad_pyramid, go, grad_camera, false, st);
 }
 
 int trips_read_stats(const trips_plan* p, const void* ws, trips_stats* out, void* stream)
@@ -423,15 +473,26 @@ int trips_read_stats(const trips_plan* p, const void* ws, trips_stats* out, void
 int trips_debug_export(const trips_plan* p, const void* ws, int32_t what, void* dst, void* stream)
 {
     if (!p || !ws || !dst) return TRIPS_ERR_ARG;
-    if (what != TRIPS_EXPORT_COUNTS && what != TRIPS_EXPORT_KEPT && what != TRIPS_EXPORT_KEPT_LAYER)
+    if (what != TRIPS_EXPORT_COUNTS && what != TRIPS_EXPORT_KEPT && what != TRIPS_EXPORT_KEPT_LAYER &&
+        what != TRIPS_EXPORT_SCREEN_GRADS)
         return TRIPS_ERR_ARG;
     if (ws != p->ws_bound || p->stage < 2) return TRIPS_ERR_STATE;
     if (what != TRIPS_EXPORT_COUNTS && p->stage != 2) return TRIPS_ERR_STATE;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     Params P = make_params(p, const_cast<void*>(ws));
-    k_export<<<p->T, kTilePix, 0, st>>>(P, what, dst);
-    int rc = check_launch();
-    if (rc) return rc;
+    int rc;
+    if (what == TRIPS_EXPORT_SCREEN_GRADS) {
+        if (!p->last_gpyr) return TRIPS_ERR_STATE;
+        if (!aligned(dst, 4)) return TRIPS_ERR_ALIGN;
+        if ((rc = cuda_status(cudaMemsetAsync(dst, 0, (size_t)p->n * (4 + p->F) * sizeof(float), st)))) return rc;
+        GradOut go;
+        memset(&go, 0, sizeof(go));
+        go.screen = static_cast<float*>(dst);
+        if ((rc = launch_backward(p, P, p->last_gpyr, go, nullptr, true, st))) return rc;
+    } else {
+        k_export<<<p->T, kTilePix, 0, st>>>(P, what, dst);
+        if ((rc = check_launch())) return rc;
+    }
     return cuda_status(cudaStreamSynchronize(st));
 }
 
@@ -575,6 +636,43 @@ int trips_morton_order(void* ws, int64_t n, const float* pos, int32_t* perm_out,
         if ((rc = check_launch())) return rc;
     }
     return TRIPS_OK;
+}
+
+int trips_microbench(int32_t op, int32_t pattern, void* buf, int64_t bytes, int32_t row_bytes, int64_t ops, void* stream,
+                     double* ms_out, int64_t* ops_done)
+{
+    if (op < kMbRedV4 || op > kMbLdV4 || (pattern != 0 && pattern != 1) || !buf || !ms_out || ops <= 0)
+        return TRIPS_ERR_ARG;
+    if (row_bytes < 16 || row_bytes % 16 || bytes < (int64_t)row_bytes * 64) return TRIPS_ERR_ARG;
+    if (!aligned(buf, 16)) return TRIPS_ERR_ALIGN;
+    uint64_t rows = 1;
+    while (rows * 2 * (uint64_t)row_bytes <= (uint64_t)bytes) rows *= 2;
+    const int blocks = num_sms() * 8, threads = 256;
+    const int64_t tot = (int64_t)blocks * threads;
+    const uint32_t iters = (uint32_t)std::max<int64_t>(1, (ops + tot - 1) / tot);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    uint32_t* sink = reinterpret_cast<uint32_t*>(buf);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, st);
+    switch (op) {
+    case kMbRedV4: k_microbench<kMbRedV4><<<blocks, threads, 0, st>>>((char*)buf, rows - 1, row_bytes, pattern, iters, 1u, sink); break;
+    case kMbRedF32: k_microbench<kMbRedF32><<<blocks, threads, 0, st>>>((char*)buf, rows - 1, row_bytes, pattern, iters, 2u, sink); break;
+    case kMbAtomU32: k_microbench<kMbAtomU32><<<blocks, threads, 0, st>>>((char*)buf, rows - 1, row_bytes, pattern, iters, 3u, sink); break;
+    case kMbStV4: k_microbench<kMbStV4><<<blocks, threads, 0, st>>>((char*)buf, rows - 1, row_bytes, pattern, iters, 4u, sink); break;
+    default: k_microbench<kMbLdV4><<<blocks, threads, 0, st>>>((char*)buf, rows - 1, row_bytes, pattern, iters, 5u, sink); break;
+    }
+    int rc = check_launch();
+    cudaEventRecord(b, st);
+    float ms = 0.f;
+    if (!rc) rc = cuda_status(cudaEventSynchronize(b));
+    if (!rc) rc = cuda_status(cudaEventElapsedTime(&ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    *ms_out = ms;
+    if (ops_done) *ops_done = (int64_t)iters * tot;
+    return rc;
 }
 
 const char* trips_status_string(int status)

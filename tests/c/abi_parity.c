@@ -99,7 +99,7 @@ int main(void)
     trips_plan* plan = NULL;
     TK(trips_plan_create(&cfg, W, H, n, &plan));
     const int64_t P = trips_num_pixels(plan), PF = trips_pyramid_floats(plan);
-    const int G = trips_grad_stride(plan);
+    const int G = 5 + F;       /* flat gradient buffer [pos_size n x 4 | desc n x F | opacity n] */
 
     float *d_pos, *d_sw, *d_al, *d_de, *d_pyr, *d_gpyr, *d_grad;
     void *d_ws, *d_exp;
@@ -126,12 +126,13 @@ int main(void)
     int fails = 0;
     /* documented call-order error: backward before any forward */
     TK(trips_project(plan, d_ws, &cam, n, d_pos, d_sw, d_al, d_de, NULL, NULL, st));
-    if (trips_splat_backward(plan, d_ws, d_gpyr, d_grad, NULL, st) != TRIPS_ERR_STATE) {
+    float *d_gps = d_grad, *d_gde = d_grad + 4 * n, *d_gop = d_grad + (4 + F) * n;
+    if (trips_splat_backward(plan, d_ws, d_gpyr, d_gps, d_gop, d_gde, NULL, st) != TRIPS_ERR_STATE) {
         fprintf(stderr, "backward before forward was not rejected\n");
         ++fails;
     }
     TK(trips_splat_forward(plan, d_ws, d_pyr, TRIPS_FWD_SAVE_FOR_BACKWARD, st));
-    TK(trips_splat_backward(plan, d_ws, d_gpyr, d_grad, NULL, st));
+    TK(trips_splat_backward(plan, d_ws, d_gpyr, d_gps, d_gop, d_gde, NULL, st));
     CK(cudaStreamSynchronize(st));
 
     float* pyr = malloc(sizeof(float) * PF);
@@ -173,7 +174,9 @@ int main(void)
     for (int64_t k = 0; k < PF; ++k) bad_feat += fabs((double)pyr[k] - opyr[k]) > 1e-5 * omag[k] + 1e-30;
     for (int64_t i = 0; i < n; ++i)
         for (int c = 0; c < 5 + F; ++c) {
-            const double g = grad[i * G + c], o = og[i * (5 + F) + c], m = ogm[i * (5 + F) + c];
+            /* oracle row order (d pos, d s_w, d alpha, d tau) from the flat buffer */
+            const double g = c < 4 ? grad[4 * i + c] : (c == 4 ? grad[(4 + F) * n + i] : grad[4 * n + i * F + (c - 5)]);
+            const double o = og[i * (5 + F) + c], m = ogm[i * (5 + F) + c];
             bad_grad += fabs(g - o) > 1e-3 * m + 1e-30;
         }
     if (gst.n_frag != ost.n_frag || gst.n_kept != ost.n_kept || gst.max_list != ost.max_list) {

@@ -46,7 +46,6 @@ def test_plan_geometry(A):
     try:
         assert A.trips_num_pixels(plan) == 2_754_000          # P at 1080p, n=4
         assert A.trips_pyramid_floats(plan) == 5 * 2_754_000
-        assert A.trips_grad_stride(plan) == 12
         dims = [A.trips_layer_dims(plan, l) for l in range(4)]
         assert [(h, w) for h, w, _ in dims] == [(1080, 1920), (540, 960), (270, 480), (135, 240)]
         assert [o for _, _, o in dims] == [0, 5 * 2073600, 5 * (2073600 + 518400), 5 * (2073600 + 518400 + 129600)]
@@ -59,14 +58,14 @@ def test_plan_geometry(A):
     try:
         assert A.trips_num_pixels(plan) == 2_764_845           # P at 1080p, n=8
         small = A.trips_workspace_bytes(plan)
-        # kept lists are dense per tile, 16 slots per pixel: (8-B key + 4-B gamma) each
-        assert small >= 2_764_845 * 16 * (8 + 4)
+        # kept lists are dense per tile, 16 slots per pixel: kept-pair key (8 B) + info (4 B) + gamma (4 B)
+        assert small >= 2_764_845 * 16 * (8 + 4 + 4)
     finally:
         A.trips_plan_destroy(plan)
-    # coarse-layer inclusion: + own lists, 16 per tile pixel
+    # coarse-layer inclusion: per-pixel kept keys (8 B) + own lists (8 B) + gamma (4 B) per slot
     plan = A.trips_plan_create(8, 4, 1920, 1080, 10, 0.0, 20)
     try:
-        assert A.trips_workspace_bytes(plan) >= small + 2_764_845 * 16 * 8
+        assert A.trips_workspace_bytes(plan) >= 2_764_845 * 16 * (8 + 8 + 4)
     finally:
         A.trips_plan_destroy(plan)
 
@@ -99,10 +98,24 @@ def test_host_side_validation(A):
                               height=cam.height)
         assert A.trips_project(plan, ws, wrong, 10, 16, 16, 16, 16) == A.TRIPS_ERR_ARG
         assert A.trips_splat_forward(plan, ws, 256, 1) == A.TRIPS_ERR_STATE
-        assert A.trips_splat_backward(plan, ws, 256, 256) == A.TRIPS_ERR_STATE
+        assert A.trips_splat_backward(plan, ws, 256, 256, 256, 256) == A.TRIPS_ERR_STATE
+        assert A.trips_splat_backward(plan, ws, None, 256, 256, 256) == A.TRIPS_ERR_ARG
         assert "STATE" in A.status_string(A.TRIPS_ERR_STATE)
     finally:
         A.trips_plan_destroy(plan)
+
+
+def test_microbench_validation(A):
+    """trips_microbench rejects bad arguments before any CUDA call."""
+    import ctypes as C
+    ms, done = C.c_double(), C.c_int64()
+    L = A.lib()
+    assert L.trips_microbench(5, 0, 1 << 20, 1 << 20, 16, 1, None, C.byref(ms), C.byref(done)) == A.TRIPS_ERR_ARG
+    assert L.trips_microbench(0, 2, 1 << 20, 1 << 20, 16, 1, None, C.byref(ms), C.byref(done)) == A.TRIPS_ERR_ARG
+    assert L.trips_microbench(0, 0, 1 << 20, 1 << 20, 24, 1, None, C.byref(ms), C.byref(done)) == A.TRIPS_ERR_ARG
+    assert L.trips_microbench(0, 0, 1 << 20, 512, 16, 1, None, C.byref(ms), C.byref(done)) == A.TRIPS_ERR_ARG
+    assert L.trips_microbench(0, 0, (1 << 20) + 4, 1 << 20, 16, 1, None, C.byref(ms), C.byref(done)) == \
+        A.TRIPS_ERR_ALIGN
 
 
 def test_no_cpu_fallback_when_library_missing(A, tmp_path, monkeypatch):

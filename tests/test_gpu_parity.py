@@ -61,10 +61,8 @@ def gpu_run(sc, dev, cam=None, G=None, save=True, export=True, desc_misalign=Fal
                 out["kept_layer"] = r.export_kept_layer().cpu().numpy()
     if G is not None:
         g = r.backward(T(G, dev))
-        gg = g.cpu().numpy()
-        F = sc.F
-        out["grad"] = np.concatenate([gg[:, :5], gg[:, 5:5 + F]], 1).astype(np.float64)
-        out["grad_pad"] = gg[:, 5 + F:]
+        out["grad"] = r.grad_rows(g).cpu().numpy().astype(np.float64)
+        out["screen"] = r.export_screen_grads().cpu().numpy().astype(np.float64)
     torch.cuda.synchronize()
     return out
 
@@ -117,12 +115,17 @@ def pixel_float_index(cam, n_layers, F1, pix):
 
 def check_backward(sc, got, G, cam=None, mask=None, **var):
     cam = cam or sc.cams[0]
-    g, gm = oracle.backward(cam, sc.n_layers, sc.pos, sc.sw, sc.alpha, sc.desc, G, mask=mask, **_ovar(var))
+    scr = np.zeros((sc.n, 4 + sc.F))
+    scm = np.zeros((sc.n, 4 + sc.F))
+    g, gm = oracle.backward(cam, sc.n_layers, sc.pos, sc.sw, sc.alpha, sc.desc, G, mask=mask, screen=scr,
+                            screen_mag=scm, **_ovar(var))
     err = np.abs(got["grad"] - g)
     bad = err > GRAD_TOL * gm + 1e-30
     assert not bad.any(), f"{bad.sum()} gradient entries out of tolerance; worst rel " \
                           f"{(err / np.maximum(gm, 1e-30)).max():.3e}"
-    assert not got["grad_pad"].any()
+    if "screen" in got:                                  # SCREEN_GRADS debug export
+        serr = np.abs(got["screen"] - scr)
+        assert not (serr > GRAD_TOL * scm + 1e-30).any(), "screen-space gradients out of tolerance"
     rel_l2 = np.linalg.norm(got["grad"] - g) / max(np.linalg.norm(g), 1e-30)
     assert rel_l2 < 1e-4, rel_l2
 
@@ -221,7 +224,7 @@ def test_multi_view_accumulation(dev):
             for c in sc.cams]
     r = Rasterizer(160, 96, 4, sc.F, max_points=sc.n, device=dev)
     pos, sw, al, de = (T(a, dev) for a in (sc.pos, sc.sw, sc.alpha, sc.desc))
-    grad = torch.zeros(sc.n, r.G, device=dev)
+    grad = r.new_grad(sc.n)
     acc, accm = None, None
     for v, cam in enumerate(cams):
         G = scenes.grad_pyramid(r.pyramid_floats, seed=v)
@@ -229,8 +232,7 @@ def test_multi_view_accumulation(dev):
         r.forward(save=True)
         r.backward(T(G, dev), grad)
         acc, accm = oracle.backward(cam, 4, sc.pos, sc.sw, sc.alpha, sc.desc, G, grad=acc, grad_mag=accm)
-    gg = grad.cpu().numpy()
-    got = np.concatenate([gg[:, :5], gg[:, 5:5 + sc.F]], 1)
+    got = r.grad_rows(grad).cpu().numpy()
     assert np.all(np.abs(got - acc) <= GRAD_TOL * accm + 1e-30)
 
 
@@ -246,14 +248,13 @@ def test_batch_step_over_two_streams(dev):
     pos, sw, al, de = (T(a, dev) for a in (sc.pos, sc.sw, sc.alpha, sc.desc))
     Gs = [scenes.grad_pyramid(rasts[0].pyramid_floats, seed=v) for v in range(5)]
     Gd = [T(g, dev) for g in Gs]
-    grad = torch.full((sc.n, rasts[0].G), 7.0, device=dev)            # zeroed by the step
+    grad = torch.full((rasts[0].grad_floats(sc.n),), 7.0, device=dev)       # zeroed by the step
     tdist.cuda_batch_step(rasts, cams, pos, sw, al, de, lambda v: Gd[v], range(5), grad)
     torch.cuda.synchronize()
     acc, accm = None, None
     for v, cam in enumerate(cams):
         acc, accm = oracle.backward(cam, 4, sc.pos, sc.sw, sc.alpha, sc.desc, Gs[v], grad=acc, grad_mag=accm)
-    gg = grad.cpu().numpy()
-    got = np.concatenate([gg[:, :5], gg[:, 5:5 + sc.F]], 1)
+    got = rasts[0].grad_rows(grad, sc.n).cpu().numpy()
     assert np.all(np.abs(got - acc) <= GRAD_TOL * accm + 1e-30)
 
 
@@ -273,12 +274,13 @@ def test_streamed_steps_pipeline(dev):
     def step(dv, g):
         tdist.cuda_batch_step(rasts, cams, dv["pos"], dv["sw"], dv["alpha"], dv["desc"], G, range(3), g)
 
-    ref = torch.zeros(sc.n, rasts[0].G, device=dev)
+    nf = rasts[0].grad_floats(sc.n)
+    ref = torch.zeros(nf, device=dev)
     step({k: v.to(dev) for k, v in host.items()}, ref)
     torch.cuda.synchronize()
     ref = ref.cpu().numpy()
-    out = [torch.zeros(sc.n, rasts[0].G).pin_memory() for _ in range(2)]
-    pipe = tdist.StreamedSteps(host, torch.zeros(sc.n, rasts[0].G, device=dev), dev)
+    out = [torch.zeros(nf).pin_memory() for _ in range(2)]
+    pipe = tdist.StreamedSteps(host, torch.zeros(nf, device=dev), dev)
     pipe.run(5, step, out)
     torch.cuda.synchronize()
     for o in out:
@@ -313,7 +315,8 @@ def test_abi_error_paths(dev):
         ws = torch.empty(A.trips_workspace_bytes(plan), dtype=torch.uint8, device=dev)
         ws2 = torch.empty(A.trips_workspace_bytes(plan), dtype=torch.uint8, device=dev)
         pyr = torch.empty(A.trips_pyramid_floats(plan), device=dev)
-        grad = torch.zeros(sc.n, A.trips_grad_stride(plan), device=dev)
+        grad = torch.zeros(sc.n * (5 + sc.F), device=dev)
+        gps, gde, gop = grad.data_ptr(), grad.data_ptr() + 16 * sc.n, grad.data_ptr() + 4 * (4 + sc.F) * sc.n
         pos, sw, al, de = (T(a, dev) for a in (sc.pos, sc.sw, sc.alpha, sc.desc))
         args = (pos.data_ptr(), sw.data_ptr(), al.data_ptr(), de.data_ptr())
         assert A.trips_splat_forward(plan, ws.data_ptr(), pyr.data_ptr(), 1) == A.TRIPS_ERR_STATE
@@ -324,12 +327,14 @@ def test_abi_error_paths(dev):
         assert A.trips_project(plan, ws.data_ptr(), cam, sc.n, *args) == A.TRIPS_OK
         assert A.trips_splat_forward(plan, ws2.data_ptr(), pyr.data_ptr(), 1) == A.TRIPS_ERR_STATE
         assert A.trips_splat_forward(plan, ws.data_ptr(), pyr.data_ptr(), 0) == A.TRIPS_OK
-        assert A.trips_splat_backward(plan, ws.data_ptr(), pyr.data_ptr(), grad.data_ptr()) == A.TRIPS_ERR_STATE
+        assert A.trips_splat_backward(plan, ws.data_ptr(), pyr.data_ptr(), gps, gop, gde) == A.TRIPS_ERR_STATE
         assert A.trips_splat_forward(plan, ws.data_ptr(), pyr.data_ptr(), 1) == A.TRIPS_ERR_STATE  # needs project
         assert A.trips_project(plan, ws.data_ptr(), cam, sc.n, *args) == A.TRIPS_OK
         assert A.trips_splat_forward(plan, ws.data_ptr(), pyr.data_ptr(), 1) == A.TRIPS_OK
-        assert A.trips_splat_backward(plan, ws.data_ptr(), pyr.data_ptr(), grad.data_ptr() + 4) == A.TRIPS_ERR_ALIGN
-        assert A.trips_splat_backward(plan, ws.data_ptr(), pyr.data_ptr(), grad.data_ptr()) == A.TRIPS_OK
+        assert A.trips_splat_backward(plan, ws.data_ptr(), pyr.data_ptr(), gps + 4, gop, gde) == A.TRIPS_ERR_ALIGN
+        assert A.trips_splat_backward(plan, ws.data_ptr(), pyr.data_ptr(), gps, gop + 2, gde) == A.TRIPS_ERR_ALIGN
+        assert A.trips_splat_backward(plan, ws.data_ptr(), pyr.data_ptr(), None, gop, gde) == A.TRIPS_ERR_ARG
+        assert A.trips_splat_backward(plan, ws.data_ptr(), pyr.data_ptr(), gps, gop, gde) == A.TRIPS_OK
         torch.cuda.synchronize()
     finally:
         A.trips_plan_destroy(plan)
@@ -462,8 +467,8 @@ def _camera_grad_case(sc, dev, mask=None, seed=3):
     err = np.abs(got - gc)
     bad = err > GRAD_TOL * gcm + 1e-30
     assert not bad.any(), [(oracle.CAMERA_GRAD_NAMES[k], got[k], gc[k], gcm[k]) for k in np.nonzero(bad)[0]]
-    a = grad.cpu().numpy()
-    b = grad_nocam.cpu().numpy()
+    a = r.grad_rows(grad).cpu().numpy()
+    b = r.grad_rows(grad_nocam).cpu().numpy()
     assert np.all(np.abs(a - b) <= 1e-3 * np.abs(b) + 1e-6 * np.abs(b).max())
 
 

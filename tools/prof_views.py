@@ -26,7 +26,7 @@ cam0 = sc.cams[0]
 r = Rasterizer(cam0.width, cam0.height, sc.n_layers, sc.F, max_points=sc.n, device=dev)
 d = [torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in (sc.pos, sc.sw, sc.alpha, sc.desc)]
 G = torch.from_numpy(scenes.grad_pyramid(r.pyramid_floats)).to(dev)
-grad = torch.zeros(sc.n, r.G, device=dev)
+grad = r.new_grad(sc.n)
 for v in range(args.views):
     cam = sc.cams[v % len(sc.cams)]
     r.project(cam, *d)

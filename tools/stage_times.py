@@ -30,7 +30,7 @@ if args.order == "lib-morton":
     perm = morton_order(d[0])
     d = [a[perm].contiguous() for a in d]
 G = torch.from_numpy(scenes.grad_pyramid(r.pyramid_floats)).to(dev)
-grad = torch.zeros(sc.n, r.G, device=dev)
+grad = r.new_grad(sc.n)
 
 
 def run(nv):

@@ -27,7 +27,7 @@ perm = morton_order(d[0])
 d = [a[perm].contiguous() for a in d]
 rasts = [Rasterizer(cam0.width, cam0.height, sc.n_layers, sc.F, max_points=sc.n, device=dev) for _ in range(4)]
 G = torch.from_numpy(scenes.grad_pyramid(rasts[0].pyramid_floats)).to(dev)
-grad = torch.zeros(sc.n, rasts[0].G, device=dev)
+grad = rasts[0].new_grad(sc.n)
 streams = [torch.cuda.Stream() for _ in range(4)]
 main = torch.cuda.current_stream()
 
