@@ -213,6 +213,9 @@ __host__ __device__ constexpr int raster_dyn_smem() { return kChunk * 32; }
 // and k_coarse_blend merges it with its ancestors' lists and blends).
 enum RasterMode { kRasterPlain = 0, kRasterTmin = 1, kRasterOwn = 2 };
 
+__device__ __forceinline__ void emit_kept_pairs(const Params& P, int t, uint32_t b0, uint32_t M, const uint64_t* s_kk,
+                                                const uint64_t* s_thr, uint32_t* s_ctr);
+
 template <int FC, int MODE>
 __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P, float* __restrict__ pyramid, int save)
 {
@@ -444,12 +447,8 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
     return;
 #endif
 
-    // phase F: the sorted kept lists stored as the tile's kept (point, tile)
-    // PAIRS: a pair of the bin is kept at corner c iff its key is among the first Keff keys of
-    // that corner's pixel; its slot m there is the key's rank (binary search of the pixel's
-    // sorted list, staged in shared memory).  A point's <= 4 kept fragments in this tile then
-    // travel together: the backward gathers its record and reduces its gradient once per pair
-    // instead of once per fragment (2.8x fewer scattered L2 operations at C4).
+    // phase F: the sorted kept lists stored as the tile's kept (point, tile) pairs
+    // (emit_kept_pairs)
 #if TRIPS_BLEND_REG
     __syncthreads();                                 // other lanes may still read s_keys (phase C)
     uint64_t* s_kk = s_keys;                         // 16 x 256 keys (= kChunk * 4)
@@ -460,36 +459,58 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
     s_thr[tid] = Keff > 0 ? s_kk[(Keff - 1) * kTilePix + tid] : 0ull;
     if (tid == 0) s_warp[0] = 0;
     __syncthreads();
+    emit_kept_pairs(P, t, b0, M, s_kk, s_thr, s_warp);
+}
+
+// Kept (point, tile) pairs of tile t: a pair of the bin is kept at corner c iff its key is among
+// the first Keff keys of that corner's pixel; its slot m there is the key's rank (binary search of
+// the pixel's sorted list).  A point's <= 4 kept fragments in the tile then travel together: the
+// backward gathers its record and reduces its gradient once per pair instead of once per fragment
+// (2.8x fewer scattered L2 operations at C4).  s_kk: [m][pixel] sorted kept keys (any key > the
+// kept ones beyond Keff), s_thr: per-pixel Keff-th key (0 if Keff = 0), *s_ctr zeroed; all threads
+// call after a barrier.
+__device__ __forceinline__ void emit_kept_pairs(const Params& P, int t, uint32_t b0, uint32_t M, const uint64_t* s_kk,
+                                                const uint64_t* s_thr, uint32_t* s_ctr)
+{
+    const int tid = threadIdx.x;
     const size_t kpb = kept_base(t);
     const unsigned long long* bk = reinterpret_cast<const unsigned long long*>(P.bin_key) + b0;
     const uint16_t* bo = P.bin_orig + b0;
-    // classify one pair: kept corners and their slots; emit it if any corner is kept
-    auto pair_f = [&](bool in, uint64_t key, uint32_t o) {
-        const int q0 = (int)(o & 31u) - 1 + ((int)((o >> 5) & 31u) - 1) * kTile;
-        uint32_t info = o & 0x3ffu;
+    for (uint32_t j0 = tid; j0 < M; j0 += kPfUnroll * kTilePix) {
+        uint64_t key[kPfUnroll];
+        uint32_t o[kPfUnroll];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            const int q = q0 + (c & 1) + (c >> 1) * kTile;
-            if (in && (o & (1u << (10 + c))) && key <= s_thr[q]) {
-                const uint64_t* L = s_kk + q;
-                int p = 0;
-                p += L[(p + 7) * kTilePix] < key ? 8 : 0;
-                p += L[(p + 3) * kTilePix] < key ? 4 : 0;
-                p += L[(p + 1) * kTilePix] < key ? 2 : 0;
-                p += L[p * kTilePix] < key ? 1 : 0;
-                info |= (1u << (10 + c)) | ((uint32_t)p << (14 + 4 * c));
+        for (int u = 0; u < kPfUnroll; ++u) {
+            const uint32_t j = j0 + u * kTilePix;
+            key[u] = j < M ? __ldg(bk + j) : kKeyMax;
+            o[u] = j < M ? __ldg(bo + j) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < kPfUnroll; ++u) {
+            const int q0 = (int)(o[u] & 31u) - 1 + ((int)((o[u] >> 5) & 31u) - 1) * kTile;
+            uint32_t info = o[u] & 0x3ffu;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const int q = q0 + (c & 1) + (c >> 1) * kTile;
+                if ((o[u] & (1u << (10 + c))) && key[u] <= s_thr[q]) {
+                    const uint64_t* L = s_kk + q;
+                    int p = 0;
+                    p += L[(p + 7) * kTilePix] < key[u] ? 8 : 0;
+                    p += L[(p + 3) * kTilePix] < key[u] ? 4 : 0;
+                    p += L[(p + 1) * kTilePix] < key[u] ? 2 : 0;
+                    p += L[p * kTilePix] < key[u] ? 1 : 0;
+                    info |= (1u << (10 + c)) | ((uint32_t)p << (14 + 4 * c));
+                }
+            }
+            if (info & 0x3c00u) {
+                const uint32_t slot = atomicAdd(s_ctr, 1u);
+                P.kp_key[kpb + slot] = key[u];
+                P.kp_info[kpb + slot] = info;
             }
         }
-        if (info & 0x3c00u) {
-            const uint32_t slot = atomicAdd(&s_warp[0], 1u);
-            P.kp_key[kpb + slot] = key;
-            P.kp_info[kpb + slot] = info;
-        }
-    };
-    for (uint32_t j = tid; j < ((M + kTilePix - 1) & ~(uint32_t)(kTilePix - 1)); j += kTilePix)
-        pair_f(j < M, j < M ? __ldg(bk + j) : 0ull, j < M ? __ldg(bo + j) : 0u);
+    }
     __syncthreads();
-    if (tid == 0) P.kp_cnt[t] = s_warp[0];
+    if (tid == 0) P.kp_cnt[t] = *s_ctr;
 }
 
 // --------------------------------------------------------------------------- K4c coarse blend
