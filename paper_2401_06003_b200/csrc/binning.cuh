@@ -22,6 +22,9 @@
 
 namespace trips {
 
+#ifndef TRIPS_HIST_FULL_ROW
+#define TRIPS_HIST_FULL_ROW 1
+#endif
 constexpr int kBinThreads = 512;           // threads per binning CTA
 #ifndef TRIPS_BIN_CTAS
 #define TRIPS_BIN_CTAS 3
@@ -172,7 +175,12 @@ __global__ void __launch_bounds__(kBinThreads, kBinCtasPerSm) k_count(Params P, 
         int t = k + rot;
         if (t >= P.T) t -= P.T;
         const uint32_t c = s_hist[t];
+#if TRIPS_HIST_FULL_ROW
+        // every entry written (untouched tiles: 0), so k_emit reads no uninitialised memory
+        row[t] = c ? atomicAdd(&P.tile_off[t], c) : 0u;
+#else
         if (c) row[t] = atomicAdd(&P.tile_off[t], c);
+#endif
     }
     if (threadIdx.x == 0) P.cta_vis[blockIdx.x] = s_v;
 }
@@ -215,7 +223,7 @@ __global__ void __launch_bounds__(kBinThreads, kBinCtasPerSm) k_emit(Params P)
 {
     extern __shared__ __align__(16) uint32_t s_cur[];             // [T] fill cursors
     const uint32_t* row = P.hist + (size_t)blockIdx.x * P.T;
-    // entries of tiles this CTA never touches are garbage and never used
+    // entries of tiles this CTA never touches are 0 (TRIPS_HIST_FULL_ROW) and never used
 #pragma unroll 8
     for (int t = threadIdx.x; t < P.T; t += blockDim.x) s_cur[t] = P.tile_off[t] + row[t];
     __syncthreads();

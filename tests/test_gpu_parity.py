@@ -375,6 +375,48 @@ def test_full_size_sampled(dev, name):
         check_backward(sc, got, G, mask=mask)
 
 
+def test_c2_whole_frame_forward(dev):
+    """C2 (5M points, 1080p, forward only) compared on EVERY pyramid pixel: counts, kept lists,
+    statistics bit-exact and all features within tolerance (no pixel sampling)."""
+    sc = scenes.make_config("C2")
+    got = gpu_run(sc, dev, save=True)
+    check_forward(sc, got)
+
+
+def test_c4_full_size_bench_layout(dev):
+    """C4 at full size in the bench launch layout: 8M points in Morton order,
+    views spread over two CUDA streams with one plan + workspace each, gradients of two views
+    accumulated into one flat buffer by dist.cuda_batch_step.  The oracle (full lists, every pixel)
+    checks view 0's counts, kept lists and features bit-exact / within tolerance, and EVERY point's
+    gradient summed over both views (full-frame upstream gradients)."""
+    from paper_2401_06003_b200 import Rasterizer
+    from paper_2401_06003_b200 import dist as tdist
+    sc = scenes.make_config("C4", order="morton")        # generator-side Morton layout (no CUDA-made input)
+    views = [0, 17]
+    cam0 = sc.cams[0]
+    rasts = [Rasterizer(cam0.width, cam0.height, sc.n_layers, sc.F, max_points=sc.n, device=dev) for _ in range(2)]
+    streams = [torch.cuda.current_stream(), torch.cuda.Stream(device=dev)]
+    pos, sw, al, de = (T(a, dev) for a in (sc.pos, sc.sw, sc.alpha, sc.desc))
+    Gs = {v: scenes.grad_pyramid(rasts[0].pyramid_floats, seed=200 + v) for v in views}
+    Gd = {v: T(g, dev) for v, g in Gs.items()}
+    grad = rasts[0].new_grad(sc.n)
+    tdist.cuda_batch_step(rasts, sc.cams, pos, sw, al, de, lambda v: Gd[v], views, grad, streams=streams)
+    torch.cuda.synchronize()
+    got_grad = rasts[0].grad_rows(grad).cpu().numpy().astype(np.float64)
+    # view 0's forward state (the forward is deterministic, so this is the step's view 0)
+    got = gpu_run(sc, dev, cam=sc.cams[0], save=True)
+    check_forward(sc, got, cam=sc.cams[0])
+    acc, accm = None, None
+    for v in views:
+        acc, accm = oracle.backward(sc.cams[v], sc.n_layers, sc.pos, sc.sw, sc.alpha, sc.desc, Gs[v], grad=acc,
+                                    grad_mag=accm)
+    err = np.abs(got_grad - acc)
+    bad = err > GRAD_TOL * accm + 1e-30
+    assert not bad.any(), f"{bad.sum()} of {bad.size} gradient entries out of tolerance"
+    assert np.linalg.norm(got_grad - acc) / np.linalg.norm(acc) < 1e-4
+    assert np.count_nonzero(acc[:, 5]) > 0.5 * sc.n          # most points received a gradient
+
+
 def test_2k_relation_full_size(dev):
     """P5 at full scale, GPU only: doubling (fx, fy, cx, cy, f, W, H) and adding a layer maps
     layer l of the original onto layer l+1 bit for bit (counts, kept lists, features)."""
