@@ -5,16 +5,22 @@ and splatted points/s at 1080p, HBM GB/s vs peak, 1/2/4/8-GPU scaling).
 Workload (BASELINE.json configs[3], "C4"): a batch of 32 camera views of an 8M-point
 Tanks&Temples-like synthetic cloud at 1920x1080, 4 pyramid layers, F = 4.  One step =
 for every view of this rank: project -> splat forward (saved) -> splat backward into
-one packed gradient buffer; then one NCCL all-reduce (SUM) of that buffer across ranks.
-Views are sharded r::N over ranks (strong scaling: the batch is fixed).
+one flat gradient buffer; then one NCCL reduction (SUM) of that buffer across ranks,
+issued asynchronously so that step k's reduction overlaps step k+1's views (double-
+buffered gradients).  Views are sharded r::N over ranks (strong scaling: the batch is fixed).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl cuda|reference]
   torchrun --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
 
-Rank 0 prints ONE JSON line.  `--impl reference` times the CPU oracle (oracle/) on a
-bounded sample of the same workload (the one other place bench.py may execute oracle/).
+Rank 0 prints ONE JSON line.  Besides the contract keys it carries a per-kernel table
+(`kernels`), the dominant kernel's `roofline` (chosen by serialised time) with its gradient
+reductions against the measured reduction ceiling (`roofline.atomics`), the other configs
+C2/C3/C5 (`configs`) and the CPU oracle timed on all host cores (`cpu_baseline`).
+`--impl reference` times the CPU oracle (oracle/) on a bounded sample of the same workload
+(the one other place bench.py may execute oracle/).
 """
 import argparse
+import concurrent.futures as cf
 import json
 import os
 import statistics
@@ -32,7 +38,11 @@ METRIC = "fwd+bwd frames/s and splatted points/s at 1080p; HBM GB/s vs peak; 1/2
 UNIT = "frames/s"
 N_POINTS = 8_000_000
 N_VIEWS = 32
-SAMPLE_ROWS = 4          # oracle sample: 4 strips of 32 rows (one per 1/4 band), time scaled x1080/128
+STRIP = 32                     # oracle sample: horizontal strips of 32 pixel rows
+# timing stages of libtrips (trips_read_stage_ms) and the kernel each one brackets
+KERNEL_OF = {"count": "k_count", "tscan": "k_tscan", "emit": "k_emit", "raster": "k_raster",
+             "backward": "k_backward_pairs"}
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "dram_traffic_r02.json")
 
 
 def peaks():
@@ -42,6 +52,27 @@ def peaks():
         return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def host_info():
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_count": os.cpu_count(), "model": model, "OMP_NUM_THREADS": os.environ.get("OMP_NUM_THREADS")}
+
+
+def dram_traffic():
+    try:
+        with open(TRAFFIC_FILE) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
 
 
 # ------------------------------------------------------------------ clocks
@@ -93,9 +124,9 @@ class ClockSampler:
 
 # ------------------------------------------------------------------ algorithmic bytes
 
-def alg_bytes(st, n, F, P):
-    """Algorithmic bytes per view (SURVEY.md 8(d) per-unit figures), attributed to the kernel
-    whose stage consumes / produces them:
+def alg_bytes(st, n, F, P, backward=True):
+    """Algorithmic bytes per view (SURVEY.md 8(d) per-unit figures, DESIGN.md "Algorithmic
+    bytes"), attributed to the kernel whose stage consumes / produces them:
       forward : 16 N (pos, s_w) | (4+4F) N_vis (alpha, tau) | 16 N_frag ((z, i) lists written
                 and read) | 8 P (counts, offsets) | 4 (F+1) P (pyramid) | 4 N_kept (saved list)
       backward: 4 (F+1) P (grad pyramid) | 4 N_kept + 4 P (saved list, offsets) |
@@ -103,50 +134,67 @@ def alg_bytes(st, n, F, P):
                 4 (5+F) N (world gradients)
     st: trips stats of the view (n_visible, n_frag, n_kept)."""
     nv, nf, nk = st["n_visible"], st["n_frag"], st["n_kept"]
-    k = {}
-    k["count"] = 16 * n
-    k["emit"] = 8 * nf
-    k["raster"] = (4 + 4 * F) * nv + 8 * nf + 8 * P + 4 * (F + 1) * P + 4 * nk
+    k = {"count": 16 * n, "tscan": 0, "emit": 8 * nf,
+         "raster": (4 + 4 * F) * nv + 8 * nf + 8 * P + 4 * (F + 1) * P + (4 * nk if backward else 0)}
     k["backward"] = (4 * (F + 1) * P + 4 * nk + 4 * P + (20 + 4 * F) * nv + 8 * (5 + F) * nv
-                     + 4 * (5 + F) * n)
-    k["sort"] = 0
+                     + 4 * (5 + F) * n) if backward else 0
     return k
 
 
 # ------------------------------------------------------------------ CPU oracle sample
 
-def oracle_sample(sc, cam, rows=SAMPLE_ROWS, phase=0, seed=100, strip=32):
-    """One view forward+backward of the oracle on `rows` horizontal strips of `strip` pixel rows,
-    one strip per 1/`rows` band of the image, each a crop camera (same intrinsics, cy shifted by
-    a multiple of 2^(n-1) so every layer's pixel grid is the full image's) over the points that
-    can reach it (a generous numpy pre-filter; sample selection only).  Returns the oracle's
-    seconds scaled by H / (rows * strip), the pixel fraction."""
+def oracle_strip_tasks(sc, cams, n_tasks, seed=100, phase=0):
+    """Inputs of n_tasks oracle runs, each the forward+backward of one STRIP-row strip of a view
+    (a crop camera with the same intrinsics, cy shifted by a multiple of 2^(n-1) so that every
+    layer's pixel grid is the full image's) over the points that can reach it (a generous numpy
+    pre-filter: sample selection only, not timed).  One view per call (cams[phase]); the strips
+    walk its image bands."""
     from oracle import oracle
     from synth import scenes
+    tasks = []
+    cam = cams[phase % len(cams)]
     H = cam.height
-    band = H // rows
     align = 1 << (sc.n_layers - 1)
+    bands = H // STRIP
     p = sc.pos.astype(np.float64) @ cam.R.astype(np.float64).T + cam.t.astype(np.float64)
-    total = 0.0
-    for b in range(rows):
-        y0 = (b * band + (phase * 37) % max(band - strip, 1)) // align * align
+    with np.errstate(all="ignore"):
+        u = cam.fx * p[:, 0] / p[:, 2] + cam.cx
+        v = cam.fy * p[:, 1] / p[:, 2] + cam.cy
+        margin = 64 + 2 * cam.f * sc.sw / p[:, 2]
+        ok = (p[:, 2] > cam.near) & (u > -margin) & (u < cam.width + margin)
+    del p, u
+    for t in range(n_tasks):
+        y0 = ((phase * 7 + t * 13) % bands) * STRIP // align * align
         crop = scenes.Camera(fx=cam.fx, fy=cam.fy, cx=cam.cx, cy=cam.cy - y0, f=cam.f, R=cam.R, t=cam.t,
-                             width=cam.width, height=strip, near=cam.near)
+                             width=cam.width, height=STRIP, near=cam.near)
         with np.errstate(all="ignore"):
-            u = cam.fx * p[:, 0] / p[:, 2] + cam.cx
-            v = cam.fy * p[:, 1] / p[:, 2] + crop.cy
-            margin = 64 + 2 * cam.f * sc.sw / p[:, 2]
-            keep = (p[:, 2] > cam.near) & (u > -margin) & (u < cam.width + margin) & (v > -margin) & \
-                (v < strip + margin)
+            keep = ok & (v - y0 > -margin) & (v - y0 < STRIP + margin)
         idx = np.nonzero(keep)[0]
-        pos, sw, al, de = sc.pos[idx], sc.sw[idx], sc.alpha[idx], sc.desc[idx]
         P = oracle.num_pixels(crop.width, crop.height, sc.n_layers)
-        G = scenes.grad_pyramid(P * (sc.F + 1), seed=seed + b)
-        t0 = time.perf_counter()
-        oracle.forward(crop, sc.n_layers, pos, sw, al, de, want_kept=False)
-        oracle.backward(crop, sc.n_layers, pos, sw, al, de, G)
-        total += time.perf_counter() - t0
-    return total * H / (rows * strip)
+        tasks.append((crop, sc.n_layers, sc.pos[idx], sc.sw[idx], sc.alpha[idx], sc.desc[idx],
+                      scenes.grad_pyramid(P * (sc.F + 1), seed=seed + t)))
+    return tasks
+
+
+def _oracle_task(task):
+    from oracle import oracle
+    crop, nl, pos, sw, al, de, G = task
+    oracle.forward(crop, nl, pos, sw, al, de, want_kept=False)
+    oracle.backward(crop, nl, pos, sw, al, de, G)
+
+
+def oracle_frames_per_s(tasks, threads, H):
+    """The oracle as it stands, on `threads` host threads (one task each at a time; the ctypes
+    calls release the GIL): frames/s = (strip rows processed / H) / wall seconds."""
+    t0 = time.perf_counter()
+    with cf.ThreadPoolExecutor(max_workers=threads) as ex:
+        list(ex.map(_oracle_task, tasks))
+    wall = time.perf_counter() - t0
+    return len(tasks) * STRIP / H / wall, wall
+
+
+def cpu_threads():
+    return max(1, int(os.environ.get("OMP_NUM_THREADS") or os.cpu_count() or 1))
 
 
 def run_reference(args, rank, world):
@@ -156,25 +204,128 @@ def run_reference(args, rank, world):
     # lib-morton: the same Morton layout, computed by the generator (the oracle has no GPU)
     sc = scenes.make_config("C4", n=N_POINTS, n_views=N_VIEWS,
                             order="morton" if args.order == "lib-morton" else args.order)
+    H = sc.cams[0].height
+    thr = cpu_threads()
+    per_step = 2 * thr
     for w in range(args.warmup):
-        oracle_sample(sc, sc.cams[w % N_VIEWS], phase=w)
-    times = [oracle_sample(sc, sc.cams[(args.warmup + k) % N_VIEWS], phase=k) for k in range(args.steps)]
-    t_view = sum(times) / len(times)                  # seconds per full view (scaled)
-    value = 1.0 / t_view
-    sample = ("per step: 1 view of C4 (8M points, 1920x1080, n=4, F=4), oracle forward+backward on 4 strips "
-              "of 32 pixel rows (one per 1/4 band; crop cameras over the points that can reach them), "
-              "time x1080/128; single thread")
+        oracle_frames_per_s(oracle_strip_tasks(sc, sc.cams, thr, phase=1000 + w), thr, H)
+    vals, walls = [], []
+    for k in range(args.steps):
+        v, wall = oracle_frames_per_s(oracle_strip_tasks(sc, sc.cams, per_step, phase=k * per_step), thr, H)
+        vals.append(v)
+        walls.append(wall)
+    value = len(vals) / sum(1.0 / v for v in vals)
+    sample = (f"per step: {per_step} strips of {STRIP} pixel rows of C4 views (8M points, 1920x1080, n=4, F=4; "
+              f"crop cameras over the points that can reach them), oracle forward+backward, {thr} host threads; "
+              f"frames/s = rows processed / 1080 / wall seconds")
+    info = host_info()
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_view * 1e3 * N_VIEWS,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(walls) / len(walls),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic", "config": {"workload": "C4: 32 views x 8M points, 1920x1080, 4 layers, F=4",
                                              "point_order": args.order},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": thr, "kind": "oracle", "sample": sample,
+                             "host": info},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 # ------------------------------------------------------------------ CUDA arm
+
+def stage_ms_per_view(torch, r, cam, inputs, views_n, backward=True, gp=None, gbuf=None):
+    """Single-stream per-stage device ms per view (libtrips' CUDA events on the launching stream),
+    after 2 warm-up views; also the view's stats."""
+    def one():
+        r.project(cam, *inputs)
+        r.forward(save=backward)
+        if backward:
+            r.backward(gp, gbuf)
+    for _ in range(2):
+        one()
+    torch.cuda.synchronize()
+    r.stage_ms(reset=True)
+    r.set_profiling(True)
+    for _ in range(views_n):
+        one()
+    torch.cuda.synchronize()
+    st = r.stage_ms(reset=True)
+    r.set_profiling(False)
+    return {k: st[k][0] / views_n for k in KERNEL_OF}, r.stats()
+
+
+def kernel_table(ms_alone, ms_step, bytes_, traffic, peak):
+    """Per-kernel algorithmic bytes, ncu DRAM bytes, times and roofline fractions (per launch)."""
+    out = {}
+    for k, kern in KERNEL_OF.items():
+        t = ms_alone.get(k)
+        if not t:
+            continue
+        row = {"kernel": kern, "alg_bytes": bytes_[k], "ms_alone": t,
+               "alg_GBps_alone": bytes_[k] / (t * 1e-3) / 1e9, "alg_frac_alone": bytes_[k] / (t * 1e-3) / 1e9 / peak}
+        if ms_step and ms_step.get(k):
+            row["ms_in_step"] = ms_step[k]
+            row["alg_frac_in_step"] = bytes_[k] / (ms_step[k] * 1e-3) / 1e9 / peak
+        d = (traffic or {}).get(kern)
+        if d:
+            row["dram_bytes"] = d
+            row["dram_GBps_alone"] = d / (t * 1e-3) / 1e9
+            row["dram_frac_alone"] = d / (t * 1e-3) / 1e9 / peak
+        out[k] = row
+    return out
+
+
+def run_configs(torch, dev, peak, traffic, views_n=8):
+    """C2 (forward only), C3, C5 (forward + backward) at full size, one stream, library Morton
+    layout: per-view stage times, frames/s, points/s, algorithmic and DRAM fractions."""
+    from paper_2401_06003_b200 import Rasterizer, morton_order
+    from synth import scenes
+    out = {}
+    for name in ("C2", "C3", "C5"):
+        sc = scenes.make_config(name)
+        cam = sc.cams[0]
+        d = [torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in (sc.pos, sc.sw, sc.alpha, sc.desc)]
+        perm = morton_order(d[0])
+        d = [a[perm].contiguous() for a in d]
+        r = Rasterizer(cam.width, cam.height, sc.n_layers, sc.F, max_points=sc.n, device=dev)
+        bwd = not sc.forward_only
+        gp = torch.from_numpy(scenes.grad_pyramid(r.pyramid_floats, seed=100)).to(dev) if bwd else None
+        gb = r.new_grad(sc.n) if bwd else None
+        ms, st = stage_ms_per_view(torch, r, cam, d, views_n, backward=bwd, gp=gp, gbuf=gb)
+        ms_view = sum(ms.values())
+        by = alg_bytes(st, sc.n, sc.F, r.P, backward=bwd)
+        tot = sum(by.values())
+        row = {"workload": f"{name}: {sc.n / 1e6:g}M points, {cam.width}x{cam.height}, {sc.n_layers} layers, F={sc.F}, "
+                           + ("fwd+bwd" if bwd else "forward only"),
+               "ms_per_view": ms_view, "frames_per_s": 1e3 / ms_view, "points_per_s": sc.n * 1e3 / ms_view,
+               "stage_ms": ms, "alg_bytes_per_view": tot, "alg_frac": tot / (ms_view * 1e-3) / 1e9 / peak,
+               "kernels": kernel_table(ms, None, by, (traffic or {}).get(name), peak), "view_stats": st,
+               "timing": f"CUDA events per stage, one stream, mean of {views_n} views after 2 warm-up"}
+        dr = sum(v.get("dram_bytes", 0) for v in row["kernels"].values())
+        if dr:
+            row["dram_GBps"] = dr / (ms_view * 1e-3) / 1e9
+            row["dram_frac"] = row["dram_GBps"] / peak
+        out[name] = row
+        del r, d, gp, gb
+        torch.cuda.empty_cache()
+    return out
+
+
+def microbench(torch, dev):
+    """Measured ceilings of 16-byte reductions (trips_microbench; tools/microbench.py has more)."""
+    from paper_2401_06003_b200 import _abi as A
+    buf = torch.zeros((2 << 30) // 4, dtype=torch.float32, device=dev)
+    st = torch.cuda.current_stream().cuda_stream
+    res = {}
+    for name, op in (("red_v4_f32", 0), ("red_f32", 1), ("atomic_add_u32", 2)):
+        for sname, nbytes in (("l2_32MB", 32 << 20), ("dram_2GB", 2 << 30)):
+            for pat, pname in ((0, "random"), (1, "coherent")):
+                A.trips_microbench(op, pat, buf.data_ptr(), nbytes, 16, 1 << 25, st)
+                best = min(A.trips_microbench(op, pat, buf.data_ptr(), nbytes, 16, 1 << 28, st)[0] for _ in range(2))
+                res[f"{name}|{sname}|{pname}"] = (1 << 28) / (best * 1e-3) / 1e9
+    del buf
+    torch.cuda.empty_cache()
+    return res
+
 
 def run_cuda(args, rank, world, local_rank):
     import torch
@@ -190,31 +341,34 @@ def run_cuda(args, rank, world, local_rank):
                             order="random" if args.order == "lib-morton" else args.order)
     n, F = sc.n, sc.F
     W, H = sc.cams[0].width, sc.cams[0].height
-    rast = Rasterizer(W, H, sc.n_layers, F, max_points=n, device=dev)
-    # views of the step are spread over args.streams CUDA streams, one plan + workspace each
-    rasts = [rast] + [Rasterizer(W, H, sc.n_layers, F, max_points=n, device=dev) for _ in range(args.streams - 1)]
+    # views of a step are spread over args.streams CUDA streams, one plan + workspace each
+    rasts = [Rasterizer(W, H, sc.n_layers, F, max_points=n, device=dev) for _ in range(args.streams)]
+    rast = rasts[0]
     streams = [torch.cuda.current_stream()] + [torch.cuda.Stream(device=dev) for _ in range(args.streams - 1)]
-    host = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory()
-            for k, v in (("pos", sc.pos), ("sw", sc.sw), ("alpha", sc.alpha), ("desc", sc.desc))}
-    d = {k: v.to(dev, non_blocking=True) for k, v in host.items()}
+    d = {k: torch.from_numpy(np.ascontiguousarray(v)).to(dev)
+         for k, v in (("pos", sc.pos), ("sw", sc.sw), ("alpha", sc.alpha), ("desc", sc.desc))}
     Gp = torch.from_numpy(scenes.grad_pyramid(rast.pyramid_floats, seed=100)).to(dev)
-    grad = rast.new_grad(n)
+    # flat gradient buffers, padded so that they split into `world` equal shards
+    gnum = tdist.padded_numel(rast.grad_floats(n), world)
+    grads = [torch.zeros(gnum, dtype=torch.float32, device=dev) for _ in range(2)]
+    shards = [torch.empty(gnum // world, dtype=torch.float32, device=dev) for _ in range(2)] \
+        if args.reduce == "reduce_scatter" and world > 1 else [None, None]
     my_views = tdist.shard_views(N_VIEWS, rank, world)
     stream = torch.cuda.current_stream()
 
-    def step(dv, grad_buf):
-        tdist.cuda_batch_step(rasts, sc.cams, dv["pos"], dv["sw"], dv["alpha"], dv["desc"], Gp, my_views, grad_buf,
-                              world=world, streams=streams)
+    def step(dv, g, out=None):
+        return tdist.cuda_batch_step(rasts, sc.cams, dv["pos"], dv["sw"], dv["alpha"], dv["desc"], Gp, my_views, g,
+                                     world=world, streams=streams, reduce=args.reduce, out=out, async_op=world > 1)
 
     def timed_ms(dv, steps):
         """device ms per step (CUDA events on the launching stream), max over ranks"""
+        pipe = tdist.PipelinedSteps(grads)
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        for _ in range(steps):
-            step(dv, grad)
+        pipe.run(steps, lambda g, k: step(dv, g, shards[k % 2]))
         b.record(stream)
         torch.cuda.synchronize()
         t = torch.tensor([a.elapsed_time(b) / steps], dtype=torch.float64, device=dev)
@@ -227,7 +381,7 @@ def run_cuda(args, rank, world, local_rank):
         if not args.no_random_order:
             # side measurement: the same workload in the generator's (random) point order
             for _ in range(2):
-                step(d, grad)
+                step(d, grads[0])
             ms_r = timed_ms(d, 3)
             random_order = {"value": N_VIEWS / (ms_r * 1e-3), "ms_per_step": ms_r, "steps": 3, "warmup": 2}
         # one-time data layout at load: the library's Morton permutation applied to every
@@ -235,7 +389,6 @@ def run_cuda(args, rank, world, local_rank):
         from paper_2401_06003_b200 import morton_order
         perm = morton_order(d["pos"])
         d = {k: v[perm].contiguous() for k, v in d.items()}
-        host = {k: v.cpu().pin_memory() for k, v in d.items()}
 
     # per-view statistics (deterministic; read outside the timed region)
     view_stats = []
@@ -246,7 +399,7 @@ def run_cuda(args, rank, world, local_rank):
     torch.cuda.synchronize()
 
     for _ in range(args.warmup):
-        step(d, grad)
+        step(d, grads[0])
     torch.cuda.synchronize()
 
     # ---- device-timed region: inputs resident in HBM
@@ -255,17 +408,7 @@ def run_cuda(args, rank, world, local_rank):
         r_.set_profiling(True)
     l0 = _abi.trips_launch_count()
     clocks = ClockSampler(local_rank)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        step(d, grad)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    ms_max = timed_ms(d, args.steps) * args.steps
     clk = clocks.stop()
     launches = _abi.trips_launch_count() - l0
     stage = {}
@@ -274,11 +417,11 @@ def run_cuda(args, rank, world, local_rank):
         for k_, (ms_, la_) in r_.stage_ms(reset=True).items():
             a_ = stage.get(k_, (0.0, 0))
             stage[k_] = (a_[0] + ms_, a_[1] + la_)
-    ms = e0.elapsed_time(e1)
-    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-    ms_max = float(ms_t.item())
+
+    # ---- every kernel alone (one stream): serialised per-launch times, the dominant kernel
+    inputs = (d["pos"], d["sw"], d["alpha"], d["desc"])
+    gb = rast.new_grad(n)
+    alone, _ = stage_ms_per_view(torch, rast, sc.cams[my_views[0]], inputs, 8, True, Gp, gb)
 
     # ---- side measurement: backward with the camera gradient
     gcam = torch.zeros(17, dtype=torch.float32, device=dev)
@@ -287,9 +430,9 @@ def run_cuda(args, rank, world, local_rank):
         rast.stage_ms(reset=True)
         rast.set_profiling(True)
         for v in my_views[:8]:
-            rast.project(sc.cams[v], d["pos"], d["sw"], d["alpha"], d["desc"])
+            rast.project(sc.cams[v], *inputs)
             rast.forward(save=True)
-            rast.backward(Gp, grad, grad_camera=gcam if with_cam else None)
+            rast.backward(Gp, gb, grad_camera=gcam if with_cam else None)
         torch.cuda.synchronize()
         st_ = rast.stage_ms(reset=True)
         rast.set_profiling(False)
@@ -298,22 +441,22 @@ def run_cuda(args, rank, world, local_rank):
     # ---- side measurement: blend variants and feature counts, per view
     def per_view_ms(r, desc, views):
         gp = torch.from_numpy(scenes.grad_pyramid(r.pyramid_floats, seed=100)).to(dev)
-        gb = r.new_grad(n)
+        g = r.new_grad(n)
         for v in views[:2]:                                          # warm-up
             r.project(sc.cams[v], d["pos"], d["sw"], d["alpha"], desc)
             r.forward(save=True)
-            r.backward(gp, gb)
+            r.backward(gp, g)
         torch.cuda.synchronize()
         r.stage_ms(reset=True)
         r.set_profiling(True)
         for v in views:
             r.project(sc.cams[v], d["pos"], d["sw"], d["alpha"], desc)
             r.forward(save=True)
-            r.backward(gp, gb)
+            r.backward(gp, g)
         torch.cuda.synchronize()
         st_ = r.stage_ms(reset=True)
         r.set_profiling(False)
-        out = {k: st_[k][0] / len(views) for k in ("count", "emit", "raster", "backward")}
+        out = {k: st_[k][0] / len(views) for k in KERNEL_OF}
         out["total"] = sum(out.values())
         return out
 
@@ -344,104 +487,131 @@ def run_cuda(args, rank, world, local_rank):
     torch.cuda.synchronize()
     knn_ms = k0.elapsed_time(k1) / 3
 
-    # ---- end to end through the public API: pinned host inputs in, gradients out
-    # (dist.StreamedSteps: double-buffered, copies on their own streams overlap the kernels)
-    out_host = [torch.empty(rast.grad_floats(n), dtype=torch.float32).pin_memory() for _ in range(2)]
-    h2d = sum(v.numel() * v.element_size() for v in host.values())
-    d2h = out_host[0].numel() * out_host[0].element_size()
-    pipe = tdist.StreamedSteps(host, grad, dev)
-    pipe.run(2, step, out_host)                                      # warm the pipeline buffers
+    # ---- end to end through the public API: pinned host inputs in, gradients out.  Each rank
+    # uploads its 1/N slice of the flat input buffer (+ NCCL all-gather) and downloads its 1/N
+    # shard of the reduce-scattered gradients (dist.ShardedStreamedSteps; at N = 1 the whole
+    # buffers, double-buffered, copies on their own streams overlapping the kernels)
+    flat_in, _, _ = tdist.flat_inputs(d["pos"], d["sw"], d["alpha"], d["desc"], world)
+    host_flat = flat_in.cpu().pin_memory()
+    del flat_in
+    pipe = tdist.ShardedStreamedSteps(host_flat, gnum, dev, world, rank)
+    out_host = [torch.empty(pipe.ghi - pipe.glo, dtype=torch.float32).pin_memory() for _ in range(2)]
+
+    def e2e_step(dev_flat, g, out):
+        pos, sw, al, de = tdist.input_views(dev_flat, n, F)
+        tdist.cuda_batch_step(rasts, sc.cams, pos, sw, al, de, Gp, my_views, g, world=world, streams=streams,
+                              reduce="reduce_scatter", out=out)
+
+    pipe.run(2, e2e_step, out_host)                                  # warm the pipeline buffers
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     f0.record(stream)
-    pipe.run(args.steps, step, out_host)
+    pipe.run(args.steps, e2e_step, out_host)
     f1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
     e2e_ms = float(e2e_ms.item())
+    del pipe
+    torch.cuda.empty_cache()
 
-    # ---- roofline of the dominant kernel (stage events are on the launching stream)
+    # ---- measured reduction ceilings, the other configs
+    mb = microbench(torch, dev) if rank == 0 else {}
     peak, peak_src = peaks()
+    traffic = dram_traffic()
+    configs = run_configs(torch, dev, peak, traffic) if (rank == 0 and not args.no_configs) else None
+
+    if rank != 0:
+        return
+    # ---- roofline: dominant kernel by serialised time
     per_view_bytes = [alg_bytes(s, n, F, rast.P) for s in view_stats]
-    stage_ms = {k: v[0] for k, v in stage.items()}
-    stage_launch = {k: v[1] for k, v in stage.items()}
-    dom = max(("raster", "backward"), key=lambda k: stage_ms[k])     # single-kernel stages
-    dom_launch_ms = stage_ms[dom] / max(stage_launch[dom], 1)
-    dom_bytes = sum(b[dom] for b in per_view_bytes) / len(per_view_bytes)
-    achieved = dom_bytes / (dom_launch_ms * 1e-3) / 1e9
-    step_bytes = sum(sum(b.values()) for b in per_view_bytes)
+    mean_bytes = {k: sum(b[k] for b in per_view_bytes) / len(per_view_bytes) for k in KERNEL_OF}
     step_ms = ms_max / args.steps
-
-    traffic = None
-    tf = os.path.join(ROOT, "profiles", "dram_traffic.json")
-    if os.path.exists(tf):
-        try:
-            traffic = json.load(open(tf)).get(dom)
-        except Exception:
-            traffic = None
-
-    if rank == 0:
-        value = N_VIEWS / (step_ms * 1e-3)
-        line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "C4: batch of 32 views x 8M points (T&T-like), 1920x1080, 4 layers, F=4, "
-                                   "fwd+bwd, view-parallel + NCCL all-reduce of point gradients",
-                       "global_batch": N_VIEWS, "points": n, "resolution": [W, H], "layers": sc.n_layers,
-                       "features": F, "parallelism": f"views{world}", "point_order": args.order,
-                       "streams_per_gpu": args.streams,
-                       "l2": "inputs larger than L2 (288 MB of point data, 288 MB gradients per step)"},
-            "points_per_s": N_VIEWS * n / (step_ms * 1e-3),
-            "fragments_per_s": sum(s["n_frag"] for s in view_stats) * world / (step_ms * 1e-3),
-            "alg_GBps_step": step_bytes * world / (step_ms * 1e-3) / 1e9,
-            "alg_frac_step": step_bytes * world / (step_ms * 1e-3) / 1e9 / peak,
-            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "alg_bytes_per_launch": dom_bytes, "launch_ms": dom_launch_ms,
-                         "note": f"launch_ms measured inside the timed step, {args.streams} concurrent streams"},
-            "stage_ms_per_step": {k: v / args.steps for k, v in stage_ms.items()},
-            "gpu_launches": launches,
-            "gpu_launches_per_step": launches / args.steps,
-            "e2e": {"value": N_VIEWS / (e2e_ms / args.steps * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h},
-            "view_stats_mean": {k: float(np.mean([s[k] for s in view_stats])) for k in view_stats[0]},
-        }
-        alone_ms = (variants.get("plain") or {}).get(dom)
-        if alone_ms:
-            # the same kernel timed alone on one stream (side measurement, CUDA events on its
-            # stream): its own roofline fraction without the other stream's kernels sharing the SMs
-            line["roofline"]["alone"] = {"launch_ms": alone_ms, "achieved": dom_bytes / (alone_ms * 1e-3) / 1e9,
-                                         "frac": dom_bytes / (alone_ms * 1e-3) / 1e9 / peak}
-        if clk is not None:
-            line["clocks"] = clk
-        if random_order is not None:
-            line["random_point_order"] = random_order
-        line["backward_ms_per_view"] = cam_ms
-        line["variants_ms_per_view"] = variants
-        knn = {"ms": knn_ms, "points_per_s": n / (knn_ms * 1e-3)}
-        if world == 1 and not args.no_cpu_baseline:
-            from oracle import oracle as _o
-            qs = np.random.default_rng(0).choice(n, 64, replace=False)
-            t0 = time.perf_counter()
-            _o.knn4(sc.pos, queries=qs)
-            dt = time.perf_counter() - t0
-            knn["cpu_baseline"] = {"points_per_s": len(qs) / dt, "cores": 1, "kind": "oracle",
-                                   "sample": "64 query points, brute force over all 8M points"}
-        line["knn4_size_init"] = knn
-        if world == 1 and not args.no_cpu_baseline:
-            from oracle import oracle as _o  # noqa: F401  (cpu_baseline leg only)
-            t = [oracle_sample(sc, sc.cams[k], phase=k + 3) for k in range(2)]
-            v = 1.0 / (sum(t) / len(t))
-            line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-                                    "sample": "2 views of C4 (8M points), oracle fwd+bwd on 4 strips of 32 pixel "
-                                              "rows each (one per 1/4 band, crop cameras), time x1080/128; "
-                                              "single thread"}
-        print(json.dumps(line), flush=True)
+    in_step = {k: stage[k][0] / max(stage[k][1], 1) for k in KERNEL_OF if k in stage}
+    kernels = kernel_table(alone, in_step, mean_bytes, traffic.get("C4"), peak)
+    dom = max(("count", "emit", "raster", "backward"), key=lambda k: alone[k])
+    kd = kernels[dom]
+    step_bytes = sum(sum(b.values()) for b in per_view_bytes)
+    value = N_VIEWS / (step_ms * 1e-3)
+    kp = float(np.mean([s["n_kept_pairs"] for s in view_stats]))
+    reds = 3 * kp                          # per kept pair: pos_size v4 + desc v4 + opacity f32
+    red_peak = max(v for k, v in mb.items() if k.startswith("red_v4_f32")) if mb else None
+    atomics = {"kernel": "k_backward_pairs", "reductions_per_launch": reds,
+               "per": "3 per kept (point, tile) pair: red.global.add.v4.f32 (pos, s_w), .v4.f32 (tau), .f32 (alpha)",
+               "achieved_G_per_s_alone": reds / (alone["backward"] * 1e-3) / 1e9}
+    if red_peak:
+        atomics.update({"peak_G_per_s": red_peak, "frac_alone": atomics["achieved_G_per_s_alone"] / red_peak,
+                        "peak_source": "trips_microbench: best red.global.add.v4.f32 rate over L2-resident / "
+                                       "DRAM-sized x random / warp-coherent addresses", "microbench": mb})
+    roof = {"bound": "hbm", "kernel": KERNEL_OF[dom], "achieved": kd["alg_bytes"] / (in_step[dom] * 1e-3) / 1e9,
+            "peak": peak, "unit": "GB/s", "peak_source": peak_src,
+            "traffic": kd.get("dram_bytes"), "alg_bytes_per_launch": kd["alg_bytes"], "launch_ms": in_step[dom],
+            "dominant_by": "serialised (single-stream) per-launch time; achieved uses the launch time inside "
+                           f"the timed step ({args.streams} concurrent streams)",
+            "alone": {"launch_ms": alone[dom], "achieved": kd["alg_GBps_alone"], "frac": kd["alg_frac_alone"],
+                      "dram_frac": kd.get("dram_frac_alone")},
+            "atomics": atomics}
+    roof["frac"] = roof["achieved"] / peak
+    ctraffic = traffic.get("C4") or {}
+    dram_view = sum(ctraffic.get(KERNEL_OF[k], 0) for k in KERNEL_OF) if ctraffic else None
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "C4: batch of 32 views x 8M points (T&T-like), 1920x1080, 4 layers, F=4, "
+                               "fwd+bwd, view-parallel + NCCL reduction of point gradients",
+                   "global_batch": N_VIEWS, "points": n, "resolution": [W, H], "layers": sc.n_layers,
+                   "features": F, "parallelism": f"views{world}", "point_order": args.order,
+                   "streams_per_gpu": args.streams, "reduction": args.reduce + (" (async, overlapped)" if world > 1
+                                                                                else " (none at 1 GPU)"),
+                   "l2": "inputs larger than L2 (288 MB of point data, 288 MB gradients per step)"},
+        "points_per_s": N_VIEWS * n / (step_ms * 1e-3),
+        "fragments_per_s": sum(s["n_frag"] for s in view_stats) * world / (step_ms * 1e-3),
+        "alg_GBps_step": step_bytes * world / (step_ms * 1e-3) / 1e9,
+        "alg_frac_step": step_bytes * world / (step_ms * 1e-3) / 1e9 / peak,
+        "roofline": roof,
+        "kernels": kernels,
+        "stage_ms_per_step": {k: v[0] / args.steps for k, v in stage.items()},
+        "gpu_launches": launches,
+        "gpu_launches_per_step": launches / args.steps,
+        "e2e": {"value": N_VIEWS / (e2e_ms / args.steps * 1e-3), "unit": UNIT,
+                "h2d_bytes_per_step": host_flat.numel() * 4 // world,
+                "d2h_bytes_per_step": out_host[0].numel() * 4,
+                "note": "per rank: 1/N slice of the flat input buffer up (+ all-gather), 1/N shard of the "
+                        "reduce-scattered gradients down, every step"},
+        "view_stats_mean": {k: float(np.mean([s[k] for s in view_stats])) for k in view_stats[0]},
+    }
+    if dram_view:
+        line["dram_frac_view_alone"] = dram_view / (sum(alone.values()) * 1e-3) / 1e9 / peak
+    if clk is not None:
+        line["clocks"] = clk
+    if random_order is not None:
+        line["random_point_order"] = random_order
+    line["backward_ms_per_view"] = cam_ms
+    line["variants_ms_per_view"] = variants
+    line["knn4_size_init"] = {"ms": knn_ms, "points_per_s": n / (knn_ms * 1e-3)}
+    if configs:
+        line["configs"] = configs
+    if world == 1 and not args.no_cpu_baseline:
+        thr = cpu_threads()
+        tasks = oracle_strip_tasks(sc, sc.cams, 2 * thr, phase=3)
+        v, wall = oracle_frames_per_s(tasks, thr, H)
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": thr, "kind": "oracle", "wall_s": wall,
+                                "host": host_info(),
+                                "sample": f"{2 * thr} strips of {STRIP} pixel rows of C4 views (8M points, crop "
+                                          f"cameras over the points that can reach them), oracle forward+backward "
+                                          f"on {thr} host threads; frames/s = rows / 1080 / wall s"}
+        qs = np.random.default_rng(0).choice(n, 64, replace=False)
+        from oracle import oracle as _o
+        t0 = time.perf_counter()
+        _o.knn4(sc.pos, queries=qs)
+        line["knn4_size_init"]["cpu_baseline"] = {"points_per_s": len(qs) / (time.perf_counter() - t0), "cores": 1,
+                                                  "kind": "oracle",
+                                                  "sample": "64 query points, brute force over all 8M points"}
+    print(json.dumps(line), flush=True)
 
 
 def main():
@@ -453,7 +623,10 @@ def main():
     ap.add_argument("--order", default="lib-morton", choices=["random", "morton", "lib-morton"],
                     help="point order: as generated (random), numpy Morton sort, or the library's "
                          "trips_morton_order applied once at load (outside the timed region)")
+    ap.add_argument("--reduce", default="allreduce", choices=["allreduce", "reduce_scatter"],
+                    help="cross-rank gradient reduction of the timed step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the C2/C3/C5 side measurements")
     ap.add_argument("--streams", type=int, default=2,
                     help="CUDA streams (one plan + workspace each) the views of a step are spread over")
     ap.add_argument("--no-random-order", action="store_true", help="skip the random-order side measurement")

@@ -86,6 +86,8 @@ typedef struct {
     int64_t n_kept;            /* sum over pixels of min(16, list length) */
     int64_t n_trunc_pixels;    /* pixels whose list was longer than 16 */
     int64_t max_list;          /* longest per-pixel list */
+    int64_t n_kept_pairs;      /* (point, tile) pairs with >= 1 kept fragment (the backward's
+                                  reduction units; 0 with coarse_layers > 0) */
 } trips_stats;
 
 typedef enum {
@@ -203,7 +205,8 @@ int trips_read_stats(const trips_plan* plan, const void* ws, trips_stats* out, v
 int trips_debug_export(const trips_plan* plan, const void* ws, int32_t what, void* dst, void* stream);
 
 /* Per-stage device timing.  When enabled, CUDA events bracket every kernel stage
- * (0 count, 1 emit, 2 sort, 3 raster, 4 backward); trips_read_stage_ms synchronises
+ * (0 count = k_count, 1 emit = k_emit, 2 tscan = k_tscan, 3 raster = k_raster [+ k_coarse_blend],
+ * 4 backward = k_backward_pairs | k_backward_coarse); trips_read_stage_ms synchronises
  * the events and returns the accumulated milliseconds and launch counts since the last
  * reset.  Returns the number of stages written. */
 int trips_set_profiling(trips_plan* plan, int32_t enable);

@@ -24,7 +24,7 @@ TRIPS_EXPORT_KEPT = 2
 TRIPS_EXPORT_KEPT_LAYER = 3
 TRIPS_EXPORT_SCREEN_GRADS = 4
 N_STAGES = 5
-STAGE_NAMES = ("count", "emit", "sort", "raster", "backward")
+STAGE_NAMES = ("count", "emit", "tscan", "raster", "backward")
 
 
 class trips_camera(C.Structure):
@@ -41,7 +41,7 @@ class trips_config(C.Structure):
 class trips_stats(C.Structure):
     _fields_ = [("n_culled", C.c_int64), ("n_visible", C.c_int64), ("n_pairs", C.c_int64),
                 ("n_frag", C.c_int64), ("n_kept", C.c_int64), ("n_trunc_pixels", C.c_int64),
-                ("max_list", C.c_int64)]
+                ("max_list", C.c_int64), ("n_kept_pairs", C.c_int64)]
 
 
 class TripsError(RuntimeError):

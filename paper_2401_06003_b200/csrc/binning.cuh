@@ -245,9 +245,10 @@ __global__ void __launch_bounds__(kBinThreads, kBinCtasPerSm) k_emit(Params P)
 
 // On-demand statistics (trips_read_stats): reduces the per-pixel list lengths and the
 // per-CTA visible counts; nothing on the hot path touches a shared counter.
-__global__ void __launch_bounds__(256) k_stats(Params P, int ctas, int npix)
+__global__ void __launch_bounds__(256) k_stats(Params P, int ctas, int npix, int ntiles_kp)
 {
-    unsigned long long frag = 0, kept = 0, trunc = 0, mx = 0, vis = 0;
+    unsigned long long frag = 0, kept = 0, trunc = 0, mx = 0, vis = 0, kpairs = 0;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < ntiles_kp; j += gridDim.x * blockDim.x) kpairs += P.kp_cnt[j];
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < npix; j += gridDim.x * blockDim.x) {
         const unsigned long long c = P.pix_cnt[j];
         frag += c;
@@ -262,6 +263,7 @@ __global__ void __launch_bounds__(256) k_stats(Params P, int ctas, int npix)
         kept += __shfl_xor_sync(0xffffffffu, kept, o);
         trunc += __shfl_xor_sync(0xffffffffu, trunc, o);
         vis += __shfl_xor_sync(0xffffffffu, vis, o);
+        kpairs += __shfl_xor_sync(0xffffffffu, kpairs, o);
         const unsigned long long m2 = __shfl_xor_sync(0xffffffffu, mx, o);
         mx = m2 > mx ? m2 : mx;
     }
@@ -270,6 +272,7 @@ __global__ void __launch_bounds__(256) k_stats(Params P, int ctas, int npix)
         if (kept) atomicAdd(&P.stats[S_KEPT], kept);
         if (trunc) atomicAdd(&P.stats[S_TRUNC], trunc);
         if (vis) atomicAdd(&P.stats[S_VISIBLE], vis);
+        if (kpairs) atomicAdd(&P.stats[S_KPAIRS], kpairs);
         if (mx) atomicMax(&P.stats[S_MAXLIST], mx);
     }
 }

@@ -73,10 +73,10 @@ struct Params {
     uint32_t* kp_cnt;      // [T]      kept pairs per tile
     uint64_t* own;         // [T][16][256] coarse inclusion only: each pixel's own sorted top-16
     float* kept_gamma;     // [T*4096] gamma of each kept fragment (saved for the backward)
-    unsigned long long* stats;  // [8]  n_culled, n_visible, n_pairs, n_frag, n_kept, n_trunc, max_list
+    unsigned long long* stats;  // [8]  n_culled, n_visible, n_pairs, n_frag, n_kept, n_trunc, max_list, n_kept_pairs
 };
 
-enum StatIdx { S_CULLED = 0, S_VISIBLE, S_PAIRS, S_FRAG, S_KEPT, S_TRUNC, S_MAXLIST, S_COUNT };
+enum StatIdx { S_CULLED = 0, S_VISIBLE, S_PAIRS, S_FRAG, S_KEPT, S_TRUNC, S_MAXLIST, S_KPAIRS, S_COUNT };
 
 // --------------------------------------------------------------------------- exact block
 

@@ -23,7 +23,8 @@ namespace {
 std::atomic<long long> g_launches{0};
 thread_local char g_msg[256];
 
-constexpr int kStages = 5;   // 0 count, 1 emit, 2 sort, 3 raster, 4 backward (kernel groups)
+constexpr int kStages = 5;   // 0 count (k_count), 1 emit (k_emit), 2 tscan (k_tscan), 3 raster (k_raster
+                             // [+ k_coarse_blend]), 4 backward (k_backward_pairs | k_backward_coarse)
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -342,6 +343,9 @@ int trips_project(trips_plan* p, void* ws, const trips_camera* c, int64_t n, con
         StageScope sc(p, 0, st);
         TRIPS_FC_SWITCH(p->FC, (k_count<kFC><<<p->ctas, kBinThreads, hsm, st>>>(P, level_out, proj_out)));
         if ((rc = check_launch())) return rc;
+    }
+    {
+        StageScope sc(p, 2, st);
         k_tscan<<<1, 1024, hsm, st>>>(P);
         if ((rc = check_launch())) return rc;
     }
@@ -453,7 +457,8 @@ int trips_read_stats(const trips_plan* p, const void* ws, trips_stats* out, void
     int rc = cuda_status(cudaMemsetAsync(P.stats, 0, S_COUNT * 8, st));
     if (rc) return rc;
     const int npix = p->stage >= 2 ? p->T * kTilePix : 0;
-    k_stats<<<std::max(1, std::min(148 * 4, (npix + 255) / 256)), 256, 0, st>>>(P, p->ctas, npix);
+    k_stats<<<std::max(1, std::min(148 * 4, (npix + 255) / 256)), 256, 0, st>>>(P, p->ctas, npix,
+                                                                              (p->stage == 2 && !p->coarse) ? p->T : 0);
     if ((rc = check_launch())) return rc;
     rc = cuda_status(cudaMemcpyAsync(h, P.stats, sizeof(h), cudaMemcpyDeviceToHost, st));
     if (rc) return rc;
@@ -465,6 +470,7 @@ int trips_read_stats(const trips_plan* p, const void* ws, trips_stats* out, void
     out->n_pairs = (int64_t)npairs;
     out->n_frag = (int64_t)h[S_FRAG];
     out->n_kept = (int64_t)h[S_KEPT];
+    out->n_kept_pairs = (int64_t)h[S_KPAIRS];
     out->n_trunc_pixels = (int64_t)h[S_TRUNC];
     out->max_list = (int64_t)h[S_MAXLIST];
     return TRIPS_OK;

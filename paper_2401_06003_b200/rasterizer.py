@@ -87,8 +87,8 @@ class Rasterizer:
     def grad_parts(self, flat, n=None):
         """(pos_size [n, 4], desc [n, F], opacity [n]) views of a flat gradient buffer."""
         n = self.n if n is None else int(n)
-        if flat.numel() != self.grad_floats(n):
-            raise ValueError(f"gradient buffer has {flat.numel()} floats, expected (5 + F) n = {self.grad_floats(n)}")
+        if flat.numel() < self.grad_floats(n):
+            raise ValueError(f"gradient buffer has {flat.numel()} floats, expected >= (5 + F) n = {self.grad_floats(n)}")
         return (flat[:4 * n].view(n, 4), flat[4 * n:(4 + self.F) * n].view(n, self.F),
                 flat[(4 + self.F) * n:(5 + self.F) * n])
 
@@ -134,7 +134,7 @@ class Rasterizer:
         return out
 
     def backward(self, grad_pyramid, grad=None, grad_camera=None):
-        """Accumulates into the flat gradient buffer `grad` [(5 + F) n] (allocated zeroed if None)
+        """Accumulates into the flat gradient buffer `grad` [>= (5 + F) n] (allocated zeroed if None)
         and, if given, into grad_camera [17] (dR row-major, dt, dfx, dfy, dcx, dcy, df)."""
         if grad is None:
             grad = self.new_grad()
@@ -142,8 +142,11 @@ class Rasterizer:
                                ("grad_camera", grad_camera, 17)):
             if t is None and name == "grad_camera":
                 continue
+            # the flat gradient buffer may carry trailing padding (sharded reductions), never less
+            ok_n = t.numel() >= numel if (name == "grad" and isinstance(t, torch.Tensor)) else \
+                (isinstance(t, torch.Tensor) and t.numel() == numel)
             if (not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float32 or t.device != self.device
-                    or not t.is_contiguous() or t.numel() != numel):
+                    or not t.is_contiguous() or not ok_n):
                 raise ValueError(f"{name} must be a contiguous float32 tensor of {numel} elements on {self.device}")
         ps, de, op = self.grad_parts(grad)
         self._last_gpyr = grad_pyramid
