@@ -11,9 +11,10 @@
 //            pairs (Eq. 4 layers, 2x2 footprints), count them per tile in shared memory;
 //            then reserve its slice of each touched tile with ONE global atomic per (CTA,
 //            tile) on the tile total; the returned base goes to hist[c][t]
-//   k_tscan  one CTA: exclusive scan of the tile totals -> tile_off; kept-list capacity base
-//   k_emit   per CTA, same point range: re-enumerate the pairs from the screen record and
+//   k_emit   per CTA, same point range: exclusive scan of the tile totals (every CTA for itself;
+//            CTA 0 publishes tile_off), then re-enumerate the pairs from the screen record and
 //            place every pair at tile_off[t] + hist[c][t] + (shared-memory cursor)
+//   (k_tscan, a one-CTA scan kernel, replaces the in-k_emit scan when TRIPS_EMIT_SCAN = 0)
 //
 // The order of pairs inside a tile's bin is not defined; K4 orders fragments by the full
 // (z, i) key (reading Q12), so results do not depend on it.
@@ -22,6 +23,12 @@
 
 namespace trips {
 
+#ifndef TRIPS_EMIT_SCAN
+#define TRIPS_EMIT_SCAN 1
+#endif
+#ifndef TRIPS_EMIT_PREFETCH
+#define TRIPS_EMIT_PREFETCH 0
+#endif
 #ifndef TRIPS_HIST_FULL_ROW
 #define TRIPS_HIST_FULL_ROW 1
 #endif
@@ -159,7 +166,7 @@ __global__ void __launch_bounds__(kBinThreads, kBinCtasPerSm) k_count(Params P, 
     const uint32_t wv = __reduce_add_sync(0xffffffffu, nvis);
     if (lane_id() == 0 && wv) atomicAdd(&s_v, wv);
     __syncthreads();
-    // reserve this CTA's slice of every tile it touches: tile_off[t] holds the running tile
+    // reserve this CTA's slice of every tile it touches: tile_cnt[t] holds the running tile
     // total here (k_tscan turns totals into offsets); the returned value is the CTA's offset
     // inside the tile.  One atomic per (CTA, non-empty tile), spread over T addresses; every
     // CTA starts at a different tile so that CTAs finishing together do not queue on the
@@ -177,9 +184,9 @@ __global__ void __launch_bounds__(kBinThreads, kBinCtasPerSm) k_count(Params P, 
         const uint32_t c = s_hist[t];
 #if TRIPS_HIST_FULL_ROW
         // every entry written (untouched tiles: 0), so k_emit reads no uninitialised memory
-        row[t] = c ? atomicAdd(&P.tile_off[t], c) : 0u;
+        row[t] = c ? atomicAdd(&P.tile_cnt[t], c) : 0u;
 #else
-        if (c) row[t] = atomicAdd(&P.tile_off[t], c);
+        if (c) row[t] = atomicAdd(&P.tile_cnt[t], c);
 #endif
     }
     if (threadIdx.x == 0) P.cta_vis[blockIdx.x] = s_v;
@@ -196,7 +203,7 @@ __global__ void __launch_bounds__(1024) k_tscan(Params P)
     __shared__ uint32_t s_ws[32];
     const int T = P.T;
 #pragma unroll 4
-    for (int t = threadIdx.x; t < T; t += blockDim.x) s_tot[t] = P.tile_off[t];
+    for (int t = threadIdx.x; t < T; t += blockDim.x) s_tot[t] = P.tile_cnt[t];
     __syncthreads();
     const int per = (T + blockDim.x - 1) / blockDim.x;
     const int t0 = min(T, (int)threadIdx.x * per), t1 = min(T, t0 + per);
@@ -223,16 +230,61 @@ __global__ void __launch_bounds__(kBinThreads, kBinCtasPerSm) k_emit(Params P)
 {
     extern __shared__ __align__(16) uint32_t s_cur[];             // [T] fill cursors
     const uint32_t* row = P.hist + (size_t)blockIdx.x * P.T;
+#if TRIPS_EMIT_SCAN
+    // every CTA scans the tile totals itself (T independent coalesced loads, one block scan):
+    // no separate k_tscan launch; CTA 0 publishes the offsets for the raster
+    __shared__ uint32_t s_ws[32];
+    const int T = P.T;
+#pragma unroll 8
+    for (int t = threadIdx.x; t < T; t += blockDim.x) s_cur[t] = __ldcg(P.tile_cnt + t);
+    __syncthreads();
+    {
+        const int per = (T + blockDim.x - 1) / blockDim.x;
+        const int t0 = min(T, (int)threadIdx.x * per), t1 = min(T, t0 + per);
+        uint32_t sa = 0;
+        for (int t = t0; t < t1; ++t) sa += s_cur[t];
+        uint32_t ta;
+        uint32_t pa = block_excl_scan(sa, s_ws, &ta);
+        for (int t = t0; t < t1; ++t) {
+            const uint32_t a = s_cur[t];
+            s_cur[t] = pa;
+            pa += a;
+        }
+        if (blockIdx.x == 0 && threadIdx.x == 0) P.tile_off[T] = ta;
+    }
+    __syncthreads();
+    // entries of tiles this CTA never touches are 0 (TRIPS_HIST_FULL_ROW) and never used
+#pragma unroll 8
+    for (int t = threadIdx.x; t < T; t += blockDim.x) {
+        const uint32_t o = s_cur[t];
+        if (blockIdx.x == 0) P.tile_off[t] = o;
+        s_cur[t] = o + row[t];
+    }
+#else
     // entries of tiles this CTA never touches are 0 (TRIPS_HIST_FULL_ROW) and never used
 #pragma unroll 8
     for (int t = threadIdx.x; t < P.T; t += blockDim.x) s_cur[t] = P.tile_off[t] + row[t];
+#endif
     __syncthreads();
     int b, e;
     cta_range(P.n, b, e);
+#if TRIPS_EMIT_PREFETCH
+    // the next point's record is loaded while this one's pairs are placed
+    float4 nr = make_float4(0.f, 0.f, -1.f, 0.f);
+    float nz = 0.f;
+    if (b + (int)threadIdx.x < e) { nr = __ldg(P.geo + b + threadIdx.x); nz = __ldg(P.zbuf + b + threadIdx.x); }
+    for (int i = b + threadIdx.x; i < e; i += blockDim.x) {
+        const float4 r0 = nr;
+        const float z = nz;
+        if (i + (int)blockDim.x < e) { nr = __ldg(P.geo + i + blockDim.x); nz = __ldg(P.zbuf + i + blockDim.x); }
+        if (!(r0.z >= 0.f)) continue;                             // culled
+        const uint64_t key = ((uint64_t)__float_as_uint(z) << 32) | (uint32_t)i;
+#else
     for (int i = b + threadIdx.x; i < e; i += blockDim.x) {
         const float4 r0 = __ldg(P.geo + i);
         if (!(r0.z >= 0.f)) continue;                             // culled
         const uint64_t key = ((uint64_t)__float_as_uint(__ldg(P.zbuf + i)) << 32) | (uint32_t)i;
+#endif
         for_each_pair(P, r0.x, r0.y, r0.z, [&](int t, uint32_t o) {
             const uint32_t pos = atomicAdd(&s_cur[t], 1u);
             P.bin_key[pos] = key;

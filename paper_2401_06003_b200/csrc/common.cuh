@@ -59,6 +59,7 @@ struct Params {
     int32_t tau_direct;
     uint32_t* hist;        // [C][T]   per-CTA tile counts -> per-CTA offsets within the tile
     uint32_t* cta_vis;     // [C]      visible points per binning CTA (statistics)
+    uint32_t* tile_cnt;    // [T]      pairs per tile (k_count's reservations)
     uint32_t* tile_off;    // [T+1]    first pair of each tile's bin; [T] = number of pairs M
     uint64_t* bin_key;     // [8n]     (z bits << 32 | i) per (tile, pair), tile-major
     uint16_t* bin_orig;    // [8n]     footprint origin in the tile: (qx0+1) | (qy0+1) << 5

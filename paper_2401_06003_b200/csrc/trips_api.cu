@@ -43,7 +43,7 @@ struct trips_plan {
     uint64_t kcap;
     // workspace layout (byte offsets)
     int32_t ctas;           // binning CTAs (persistent grid)
-    size_t off_geo, off_tau, off_z, off_hist, off_cvis, off_toff, off_bkey, off_borig, off_pcnt, off_pmeta, off_kept, off_kgam,
+    size_t off_geo, off_tau, off_z, off_hist, off_cvis, off_toff, off_tcnt, off_bkey, off_borig, off_pcnt, off_pmeta, off_kept, off_kgam,
         off_own, off_kpkey, off_kpinfo, off_kpcnt, off_stats, ws_bytes;
     // state
     const void* ws_bound = nullptr;
@@ -185,6 +185,7 @@ Params make_params(const trips_plan* p, void* ws)
     P.hist = reinterpret_cast<uint32_t*>(b + p->off_hist);
     P.cta_vis = reinterpret_cast<uint32_t*>(b + p->off_cvis);
     P.tile_off = reinterpret_cast<uint32_t*>(b + p->off_toff);
+    P.tile_cnt = reinterpret_cast<uint32_t*>(b + p->off_tcnt);
     P.bin_key = reinterpret_cast<uint64_t*>(b + p->off_bkey);
     P.bin_orig = reinterpret_cast<uint16_t*>(b + p->off_borig);
     P.pix_cnt = reinterpret_cast<uint32_t*>(b + p->off_pcnt);
@@ -263,6 +264,7 @@ int trips_plan_create(const trips_config* cfg, int32_t width, int32_t height, in
     p->off_hist = o;   o = align256(o + (size_t)p->ctas * tiles * 4);
     p->off_cvis = o;   o = align256(o + (size_t)p->ctas * 4);
     p->off_toff = o;   o = align256(o + ((size_t)tiles + 1) * 4);
+    p->off_tcnt = o;   o = align256(o + (size_t)tiles * 4);
     p->off_bkey = o;   o = align256(o + 8 * N * 8);
     p->off_borig = o;  o = align256(o + 8 * N * 2);
     p->off_pcnt = o;  o = align256(o + (size_t)tiles * kTilePix * 4);
@@ -335,7 +337,7 @@ int trips_project(trips_plan* p, void* ws, const trips_camera* c, int64_t n, con
     P.pos = pos; P.sw = world_size; P.alpha = opacity; P.desc = desc;
     int rc = cuda_status(cudaMemsetAsync(P.stats, 0, S_COUNT * 8, st));
     if (rc) return rc;
-    rc = cuda_status(cudaMemsetAsync(P.tile_off, 0, ((size_t)p->T + 1) * 4, st));
+    rc = cuda_status(cudaMemsetAsync(P.tile_cnt, 0, (size_t)p->T * 4, st));
     if (rc) return rc;
     const size_t hsm = (size_t)p->T * 4;
     if ((rc = set_smem_attrs(hsm))) return rc;
@@ -344,11 +346,13 @@ int trips_project(trips_plan* p, void* ws, const trips_camera* c, int64_t n, con
         TRIPS_FC_SWITCH(p->FC, (k_count<kFC><<<p->ctas, kBinThreads, hsm, st>>>(P, level_out, proj_out)));
         if ((rc = check_launch())) return rc;
     }
+#if !TRIPS_EMIT_SCAN
     {
         StageScope sc(p, 2, st);
         k_tscan<<<1, 1024, hsm, st>>>(P);
         if ((rc = check_launch())) return rc;
     }
+#endif
     {
         StageScope sc(p, 1, st);
         k_emit<<<p->ctas, kBinThreads, hsm, st>>>(P);
