@@ -19,7 +19,7 @@ namespace trips {
 #define TRIPS_CHUNK 1024
 #endif
 #ifndef TRIPS_BLEND_BATCH
-#define TRIPS_BLEND_BATCH 2
+#define TRIPS_BLEND_BATCH 4
 #endif
 #ifndef TRIPS_RASTER_CTAS
 #define TRIPS_RASTER_CTAS 3
@@ -38,7 +38,7 @@ namespace trips {
 #define TRIPS_RED_CLOBBER 1
 #endif
 #ifndef TRIPS_BWD_CTAS
-#define TRIPS_BWD_CTAS 3
+#define TRIPS_BWD_CTAS 4
 #endif
 constexpr int kChunk = TRIPS_CHUNK;         // (point, tile) pairs staged per K4 iteration
 constexpr int kPairsPerThread = kChunk / kTilePix;
@@ -206,7 +206,9 @@ __device__ __forceinline__ TileCoord tile_coord(const Params& P, int t)
 // Dynamic shared memory of k_raster: the per-chunk fragment keys.  (Reusing it after the last
 // chunk to stage the kept records for the blend with one cp.async wave was measured slower:
 // 64 KB per CTA shrinks L1 -- profiles/r01_v2.md.)
-__host__ __device__ constexpr int raster_dyn_smem() { return kChunk * 32; }
+// After the last chunk the buffer holds the 16 x 256 sorted kept keys (phase D / F), so it is at
+// least 32 KB whatever the chunk size.
+__host__ __device__ constexpr int raster_dyn_smem() { return kChunk * 32 > kCap * kTilePix * 8 ? kChunk * 32 : kCap * kTilePix * 8; }
 
 // MODE: kRasterPlain (the definition), kRasterTmin (T_min variant, Q17) or kRasterOwn
 // (coarse-layer inclusion, Q22: phases A-C only; the pixel's own sorted top-16 goes to P.own
@@ -906,7 +908,7 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_BWD_CTAS) k_backward_pairs(Par
 // the blended fragments of a pixel come from several layers and tiles, so they are replayed per
 // pixel and reduced per fragment.
 template <int FC, bool CAM, bool SCREEN>
-__global__ void __launch_bounds__(kTilePix, FC <= 4 ? TRIPS_BWD_CTAS : 2) k_backward_coarse(Params P, const float* __restrict__ gpyr,
+__global__ void __launch_bounds__(kTilePix, FC <= 4 ? 3 : 2) k_backward_coarse(Params P, const float* __restrict__ gpyr,
                                                        GradOut go, float* __restrict__ grad_cam)
 {
     const int t = blockIdx.x;
