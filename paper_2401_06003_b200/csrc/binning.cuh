@@ -14,7 +14,8 @@
 //   k_emit   per CTA, same point range: exclusive scan of the tile totals (every CTA for itself;
 //            CTA 0 publishes tile_off), then re-enumerate the pairs from the screen record and
 //            place every pair at tile_off[t] + hist[c][t] + (shared-memory cursor)
-//   (k_tscan, a one-CTA scan kernel, replaces the in-k_emit scan when TRIPS_EMIT_SCAN = 0)
+//   The tile totals are scanned into tile_off by the LAST k_count CTA to finish (completion
+//   ticket; TRIPS_TILE_SCAN selects the alternatives: in every k_emit CTA, or a k_tscan launch)
 //
 // The order of pairs inside a tile's bin is not defined; K4 orders fragments by the full
 // (z, i) key (reading Q12), so results do not depend on it.
@@ -23,9 +24,12 @@
 
 namespace trips {
 
-#ifndef TRIPS_EMIT_SCAN
-#define TRIPS_EMIT_SCAN 1
+// Where the tile totals become offsets: 2 = the last k_count CTA to finish (a completion
+// ticket in tile_cnt[T]), 1 = every k_emit CTA for itself, 0 = a one-CTA k_tscan launch.
+#ifndef TRIPS_TILE_SCAN
+#define TRIPS_TILE_SCAN 2
 #endif
+#define TRIPS_EMIT_SCAN (TRIPS_TILE_SCAN == 1)
 #ifndef TRIPS_EMIT_PREFETCH
 #define TRIPS_EMIT_PREFETCH 0
 #endif
@@ -76,6 +80,32 @@ __device__ __forceinline__ void cta_range(int n, int& b, int& e)
     const int per = (n + gridDim.x - 1) / gridDim.x;
     b = min(n, (int)blockIdx.x * per);
     e = min(n, b + per);
+}
+
+// tile_off <- exclusive scan of the T tile totals (all threads of the CTA call; s_tot: >= T u32 of
+// shared memory, overwritten; s_ws: 32 u32).  Totals staged with coalesced loads (__ldcg: written
+// by other CTAs' atomics), each thread scans a contiguous run, one block scan.
+__device__ __forceinline__ void scan_tile_totals(const Params& P, uint32_t* s_tot, uint32_t* s_ws)
+{
+    const int T = P.T;
+#pragma unroll 8
+    for (int t = threadIdx.x; t < T; t += blockDim.x) s_tot[t] = __ldcg(P.tile_cnt + t);
+    __syncthreads();
+    const int per = (T + blockDim.x - 1) / blockDim.x;
+    const int t0 = min(T, (int)threadIdx.x * per), t1 = min(T, t0 + per);
+    uint32_t sa = 0;
+    for (int t = t0; t < t1; ++t) sa += s_tot[t];
+    uint32_t ta;
+    uint32_t pa = block_excl_scan(sa, s_ws, &ta);
+    for (int t = t0; t < t1; ++t) {
+        const uint32_t a = s_tot[t];
+        s_tot[t] = pa;
+        pa += a;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int t = threadIdx.x; t < T; t += blockDim.x) P.tile_off[t] = s_tot[t];
+    if (threadIdx.x == 0) P.tile_off[T] = ta;
 }
 
 // --------------------------------------------------------------------------- k_count
@@ -190,6 +220,20 @@ __global__ void __launch_bounds__(kBinThreads, kBinCtasPerSm) k_count(Params P, 
 #endif
     }
     if (threadIdx.x == 0) P.cta_vis[blockIdx.x] = s_v;
+#if TRIPS_TILE_SCAN == 2
+    // completion ticket (tile_cnt[T], zeroed with the totals): the last CTA sees every CTA's
+    // reservations and publishes the tile offsets, so k_emit starts placing pairs at once
+    __shared__ uint32_t s_last;
+    __shared__ uint32_t s_ws[32];
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(P.tile_cnt + P.T, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (s_last) {
+        __threadfence();
+        scan_tile_totals(P, s_hist, s_ws);
+    }
+#endif
 }
 
 // --------------------------------------------------------------------------- k_tscan

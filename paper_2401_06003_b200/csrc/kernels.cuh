@@ -21,6 +21,9 @@ namespace trips {
 #ifndef TRIPS_BLEND_BATCH
 #define TRIPS_BLEND_BATCH 4
 #endif
+#ifndef TRIPS_GROUP8
+#define TRIPS_GROUP8 0
+#endif
 #ifndef TRIPS_RASTER_CTAS
 #define TRIPS_RASTER_CTAS 3
 #endif
@@ -89,10 +92,37 @@ __device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float 
 
 // --------------------------------------------------------------------------- networks
 
-// Batcher odd-even merge sort networks (ascending), verified exhaustively with the 0-1
-// principle (tests/test_networks.py): 19 comparators for 8 keys, 63 for 16.
+// Sorting networks (ascending) on t[0..N), verified exhaustively with the 0-1 principle
+// (tests/test_networks.py): 5 comparators for 4 keys, 19 for 8 (Batcher odd-even merge sort),
+// 39 for 12 and 60 for 16 (the best known sizes; TRIPS_NET16 = 0 selects Batcher's 63).
+#ifndef TRIPS_NET16
+#define TRIPS_NET16 1
+#endif
+#ifndef TRIPS_NET_SIZES
+#define TRIPS_NET_SIZES 2        // network sizes k_raster phase C picks from: 2 = {8, 16}, 4 = {4, 8, 12, 16} (measured slower: +11 us)
+#endif
 template <int N>
 __device__ __forceinline__ void sort_small(uint64_t (&t)[16]);
+
+template <>
+__device__ __forceinline__ void sort_small<4>(uint64_t (&t)[16])
+{
+    cswap(t[0], t[1]); cswap(t[2], t[3]); cswap(t[0], t[2]); cswap(t[1], t[3]); cswap(t[1], t[2]);
+}
+
+template <>
+__device__ __forceinline__ void sort_small<12>(uint64_t (&t)[16])
+{
+    cswap(t[0], t[8]); cswap(t[1], t[7]); cswap(t[2], t[6]); cswap(t[3], t[11]); cswap(t[4], t[10]); cswap(t[5], t[9]);
+    cswap(t[0], t[1]); cswap(t[2], t[5]); cswap(t[3], t[4]); cswap(t[6], t[9]); cswap(t[7], t[8]); cswap(t[10], t[11]);
+    cswap(t[0], t[2]); cswap(t[1], t[6]); cswap(t[5], t[10]); cswap(t[9], t[11]);
+    cswap(t[0], t[3]); cswap(t[1], t[2]); cswap(t[4], t[6]); cswap(t[5], t[7]); cswap(t[8], t[11]); cswap(t[9], t[10]);
+    cswap(t[1], t[4]); cswap(t[3], t[5]); cswap(t[6], t[8]); cswap(t[7], t[10]);
+    cswap(t[1], t[3]); cswap(t[2], t[5]); cswap(t[6], t[9]); cswap(t[8], t[10]);
+    cswap(t[2], t[3]); cswap(t[4], t[5]); cswap(t[6], t[7]); cswap(t[8], t[9]);
+    cswap(t[4], t[6]); cswap(t[5], t[7]);
+    cswap(t[3], t[4]); cswap(t[5], t[6]); cswap(t[7], t[8]);
+}
 
 template <>
 __device__ __forceinline__ void sort_small<8>(uint64_t (&t)[16])
@@ -106,6 +136,18 @@ __device__ __forceinline__ void sort_small<8>(uint64_t (&t)[16])
 template <>
 __device__ __forceinline__ void sort_small<16>(uint64_t (&t)[16])
 {
+#if TRIPS_NET16
+    cswap(t[0], t[13]); cswap(t[1], t[12]); cswap(t[2], t[15]); cswap(t[3], t[14]); cswap(t[4], t[8]); cswap(t[5], t[6]); cswap(t[7], t[11]); cswap(t[9], t[10]);
+    cswap(t[0], t[5]); cswap(t[1], t[7]); cswap(t[2], t[9]); cswap(t[3], t[4]); cswap(t[6], t[13]); cswap(t[8], t[14]); cswap(t[10], t[15]); cswap(t[11], t[12]);
+    cswap(t[0], t[1]); cswap(t[2], t[3]); cswap(t[4], t[5]); cswap(t[6], t[8]); cswap(t[7], t[9]); cswap(t[10], t[11]); cswap(t[12], t[13]); cswap(t[14], t[15]);
+    cswap(t[0], t[2]); cswap(t[1], t[3]); cswap(t[4], t[10]); cswap(t[5], t[11]); cswap(t[6], t[7]); cswap(t[8], t[9]); cswap(t[12], t[14]); cswap(t[13], t[15]);
+    cswap(t[1], t[2]); cswap(t[3], t[12]); cswap(t[4], t[6]); cswap(t[5], t[7]); cswap(t[8], t[10]); cswap(t[9], t[11]); cswap(t[13], t[14]);
+    cswap(t[1], t[4]); cswap(t[2], t[6]); cswap(t[5], t[8]); cswap(t[7], t[10]); cswap(t[9], t[13]); cswap(t[11], t[14]);
+    cswap(t[2], t[4]); cswap(t[3], t[6]); cswap(t[9], t[12]); cswap(t[11], t[13]);
+    cswap(t[3], t[5]); cswap(t[6], t[8]); cswap(t[7], t[9]); cswap(t[10], t[12]);
+    cswap(t[3], t[4]); cswap(t[5], t[6]); cswap(t[7], t[8]); cswap(t[9], t[10]); cswap(t[11], t[12]);
+    cswap(t[6], t[7]); cswap(t[8], t[9]);
+#else
     cswap(t[0], t[1]); cswap(t[2], t[3]); cswap(t[0], t[2]); cswap(t[1], t[3]); cswap(t[1], t[2]);
     cswap(t[4], t[5]); cswap(t[6], t[7]); cswap(t[4], t[6]); cswap(t[5], t[7]); cswap(t[5], t[6]);
     cswap(t[0], t[4]); cswap(t[2], t[6]); cswap(t[2], t[4]); cswap(t[1], t[5]); cswap(t[3], t[7]);
@@ -119,6 +161,7 @@ __device__ __forceinline__ void sort_small<16>(uint64_t (&t)[16])
     cswap(t[5], t[13]); cswap(t[5], t[9]); cswap(t[3], t[11]); cswap(t[7], t[15]); cswap(t[7], t[11]);
     cswap(t[3], t[5]); cswap(t[7], t[9]); cswap(t[11], t[13]); cswap(t[1], t[2]); cswap(t[3], t[4]);
     cswap(t[5], t[6]); cswap(t[7], t[8]); cswap(t[9], t[10]); cswap(t[11], t[12]); cswap(t[13], t[14]);
+#endif
 }
 
 // r (sorted asc, 16) <- the 16 smallest of r U t, t sorted asc in t[0..N) (N = 8 or 16):
@@ -133,6 +176,23 @@ __device__ __forceinline__ void merge_keep16(uint64_t (&r)[16], const uint64_t (
 #pragma unroll
         for (int i = 0; i < 16; ++i)
             if ((i & d) == 0) cswap(r[i], r[i + d]);
+}
+
+// Phase C step: the next min(rem, N) keys of this pixel's chunk list (k[0..)) are sorted with
+// the N-key network and merged into the running top-16 r (or become it when `first`).
+template <int N>
+__device__ __forceinline__ void group_top16(uint64_t (&r)[16], const uint64_t* k, uint32_t rem, bool first)
+{
+    uint64_t tk[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) tk[j] = (j < N && (uint32_t)j < rem) ? k[j] : kKeyMax;
+    sort_small<N>(tk);
+    if (first) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) r[j] = tk[j];
+    } else {
+        merge_keep16<N>(r, tk);
+    }
 }
 
 // Exclusive prefix of one u32 per thread over a 256-thread tile CTA with a single barrier:
@@ -208,7 +268,9 @@ __device__ __forceinline__ TileCoord tile_coord(const Params& P, int t)
 // 64 KB per CTA shrinks L1 -- profiles/r01_v2.md.)
 // After the last chunk the buffer holds the 16 x 256 sorted kept keys (phase D / F), so it is at
 // least 32 KB whatever the chunk size.
-__host__ __device__ constexpr int raster_dyn_smem() { return kChunk * 32 > kCap * kTilePix * 8 ? kChunk * 32 : kCap * kTilePix * 8; }
+__host__ __device__ constexpr int raster_keys_smem() { return kChunk * 32 > kCap * kTilePix * 8 ? kChunk * 32 : kCap * kTilePix * 8; }
+
+__host__ __device__ constexpr int raster_dyn_smem() { return raster_keys_smem(); }
 
 // MODE: kRasterPlain (the definition), kRasterTmin (T_min variant, Q17) or kRasterOwn
 // (coarse-layer inclusion, Q22: phases A-C only; the pixel's own sorted top-16 goes to P.own
@@ -217,6 +279,7 @@ enum RasterMode { kRasterPlain = 0, kRasterTmin = 1, kRasterOwn = 2 };
 
 __device__ __forceinline__ void emit_kept_pairs(const Params& P, int t, uint32_t b0, uint32_t M, const uint64_t* s_kk,
                                                 const uint64_t* s_thr, uint32_t* s_ctr);
+
 
 template <int FC, int MODE>
 __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P, float* __restrict__ pyramid, int save)
@@ -328,32 +391,29 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
         // phase C: merge this pixel's new fragments into its running top-16.  Network sizes are
         // chosen per warp (8 when no lane of the warp has more than 8 keys left in the group).
         const uint32_t wcnt = __reduce_max_sync(0xffffffffu, my_cnt);
+#if TRIPS_GROUP8
+        // groups of 8 only: 16 fewer live key registers than 16-key groups (occupancy)
+        for (uint32_t g = 0; g < wcnt; g += 8) {
+            const uint32_t rem = my_cnt > g ? my_cnt - g : 0u;
+            const bool first = __all_sync(0xffffffffu, total == 0 && g == 0);
+            group_top16<8>(r, s_keys + my_base + g, rem, first);
+        }
+#else
         for (uint32_t g = 0; g < wcnt; g += 16) {
             const uint32_t rem = my_cnt > g ? my_cnt - g : 0u;
             const bool first = __all_sync(0xffffffffu, total == 0 && g == 0);
-            uint64_t tk[16];
-            if (__reduce_max_sync(0xffffffffu, rem) <= 8u) {
-#pragma unroll
-                for (int j = 0; j < 16; ++j) tk[j] = (j < 8 && (uint32_t)j < rem) ? s_keys[my_base + g + j] : kKeyMax;
-                sort_small<8>(tk);
-                if (first) {
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) r[j] = tk[j];
-                } else {
-                    merge_keep16<8>(r, tk);
-                }
-            } else {
-#pragma unroll
-                for (int j = 0; j < 16; ++j) tk[j] = ((uint32_t)j < rem) ? s_keys[my_base + g + j] : kKeyMax;
-                sort_small<16>(tk);
-                if (first) {
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) r[j] = tk[j];
-                } else {
-                    merge_keep16<16>(r, tk);
-                }
-            }
+            const uint32_t wrem = __reduce_max_sync(0xffffffffu, rem);
+#if TRIPS_NET_SIZES == 4
+            if (wrem <= 4u) group_top16<4>(r, s_keys + my_base + g, rem, first);
+            else if (wrem <= 8u) group_top16<8>(r, s_keys + my_base + g, rem, first);
+            else if (wrem <= 12u) group_top16<12>(r, s_keys + my_base + g, rem, first);
+            else group_top16<16>(r, s_keys + my_base + g, rem, first);
+#else
+            if (wrem <= 8u) group_top16<8>(r, s_keys + my_base + g, rem, first);
+            else group_top16<16>(r, s_keys + my_base + g, rem, first);
+#endif
         }
+#endif
         total += my_cnt + s_rej[tid];
         s_thr[tid] = r[15];                          // 16th smallest key so far (MAX if < 16)
         if (ch + 1 < nch) __syncthreads();           // shared buffers are reused by the next chunk only
@@ -462,6 +522,7 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
     if (tid == 0) s_warp[0] = 0;
     __syncthreads();
     emit_kept_pairs(P, t, b0, M, s_kk, s_thr, s_warp);
+    TRIPS_PCLK(7);
 }
 
 // Kept (point, tile) pairs of tile t: a pair of the bin is kept at corner c iff its key is among

@@ -19,11 +19,13 @@ namespace trips {
 constexpr int kSortBlock = 4096;            // elements per radix block (256 threads x 16 rounds)
 
 struct MortonWs {
+    using Key = uint32_t;
     uint32_t* keys[2];
     uint32_t* vals[2];
     uint32_t* hist;          // [256][nblk] digit-major -> exclusive offsets
     uint32_t* bbox;          // [6] orderable float bits: min xyz, max xyz
     int n, nblk;
+    int last_pass;           // the scatter of this pass writes the values to final_vals
 };
 
 __device__ __forceinline__ uint32_t f2ord(float f)
@@ -36,7 +38,8 @@ __device__ __forceinline__ float ord2f(uint32_t o)
     return __uint_as_float((o & 0x80000000u) ? (o & 0x7fffffffu) : ~o);
 }
 
-__global__ void __launch_bounds__(256) k_bbox(MortonWs W, const float* __restrict__ pos)
+template <typename WS>   // any workspace with n and bbox[6] (MortonWs, KnnWs)
+__global__ void __launch_bounds__(256) k_bbox(WS W, const float* __restrict__ pos)
 {
     uint32_t lo[3] = {0xffffffffu, 0xffffffffu, 0xffffffffu}, hi[3] = {0u, 0u, 0u};
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < W.n; i += gridDim.x * blockDim.x) {
@@ -94,13 +97,17 @@ __global__ void __launch_bounds__(256) k_codes(MortonWs W, const float* __restri
     W.vals[0][i] = (uint32_t)i;
 }
 
-__global__ void __launch_bounds__(256) k_sort_hist(MortonWs W, int pass)
+// Radix-sort kernels (LSD, 8 bits per pass) over any workspace WS with members Key, keys[2],
+// vals[2], hist, n, nblk, last_pass: MortonWs (30-bit codes, 4 passes) and KnnWs (48-bit cell
+// codes, 6 passes).
+template <typename WS>
+__global__ void __launch_bounds__(256) k_sort_hist(WS W, int pass)
 {
     __shared__ uint32_t h[256];
     const int blk = blockIdx.x;
     h[threadIdx.x] = 0;
     __syncthreads();
-    const uint32_t* keys = W.keys[pass & 1];
+    const typename WS::Key* keys = W.keys[pass & 1];
     for (int j = 0; j < kSortBlock / 256; ++j) {
         const int e = blk * kSortBlock + j * 256 + threadIdx.x;
         if (e < W.n) atomicAdd(&h[(keys[e] >> (8 * pass)) & 255u], 1u);
@@ -110,7 +117,8 @@ __global__ void __launch_bounds__(256) k_sort_hist(MortonWs W, int pass)
 }
 
 // One CTA: exclusive scan of the digit-major histogram (digit d, block b) in place.
-__global__ void __launch_bounds__(1024) k_sort_scan(MortonWs W)
+template <typename WS>
+__global__ void __launch_bounds__(1024) k_sort_scan(WS W)
 {
     __shared__ uint32_t ws[32];
     const int total = 256 * W.nblk;
@@ -146,24 +154,26 @@ __global__ void __launch_bounds__(1024) k_sort_scan(MortonWs W)
 
 // Stable scatter: rounds of 256 consecutive elements; rank = elements of the same digit in
 // earlier rounds + earlier warps of this round + earlier lanes of this warp.
-__global__ void __launch_bounds__(256) k_sort_scatter(MortonWs W, int pass, uint32_t* final_vals)
+template <typename WS>
+__global__ void __launch_bounds__(256) k_sort_scatter(WS W, int pass, uint32_t* final_vals)
 {
     __shared__ uint32_t base[256];           // next output position per digit
     __shared__ uint32_t wcnt[8][256];
     const int blk = blockIdx.x;
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     base[threadIdx.x] = W.hist[(size_t)threadIdx.x * W.nblk + blk];
-    const uint32_t* kin = W.keys[pass & 1];
+    using Key = typename WS::Key;
+    const Key* kin = W.keys[pass & 1];
     const uint32_t* vin = W.vals[pass & 1];
-    uint32_t* kout = W.keys[(pass + 1) & 1];
-    uint32_t* vout = (pass == 3 && final_vals) ? final_vals : W.vals[(pass + 1) & 1];
+    Key* kout = W.keys[(pass + 1) & 1];
+    uint32_t* vout = (pass == W.last_pass && final_vals) ? final_vals : W.vals[(pass + 1) & 1];
     for (int j = 0; j < kSortBlock / 256; ++j) {
 #pragma unroll
         for (int w = 0; w < 8; ++w) wcnt[w][threadIdx.x] = 0;
         __syncthreads();
         const int e = blk * kSortBlock + j * 256 + threadIdx.x;
         const bool ok = e < W.n;
-        const uint32_t k = ok ? kin[e] : 0u;
+        const Key k = ok ? kin[e] : Key(0);
         const int d = ok ? (int)((k >> (8 * pass)) & 255u) : -1;
         const unsigned peers = __match_any_sync(0xffffffffu, d);
         if (ok && lane == (unsigned)(__ffs(peers) - 1)) wcnt[warp][d] = __popc(peers);

@@ -259,8 +259,9 @@ def test_batch_step_over_two_streams(dev):
 
 
 def test_streamed_steps_pipeline(dev):
-    """dist.StreamedSteps: double-buffered host->device->host steps give every step's exact
-    gradients (same as a synchronous step) in host memory."""
+    """dist.ShardedStreamedSteps (the bench's e2e path, world 1): double-buffered host -> device
+    -> host steps through the flat input buffer give every step's exact gradients (same as a
+    synchronous step) in host memory."""
     from paper_2401_06003_b200 import Rasterizer
     from paper_2401_06003_b200 import dist as tdist
     sc = scenes.make_config("C4", n=20000, n_views=3)
@@ -268,19 +269,23 @@ def test_streamed_steps_pipeline(dev):
             for c in sc.cams]
     rasts = [Rasterizer(160, 96, 4, sc.F, max_points=sc.n, device=dev) for _ in range(2)]
     G = T(scenes.grad_pyramid(rasts[0].pyramid_floats, seed=3), dev)
-    host = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory()
-            for k, v in (("pos", sc.pos), ("sw", sc.sw), ("alpha", sc.alpha), ("desc", sc.desc))}
-
-    def step(dv, g):
-        tdist.cuda_batch_step(rasts, cams, dv["pos"], dv["sw"], dv["alpha"], dv["desc"], G, range(3), g)
-
+    dv = {k: T(v, dev) for k, v in (("pos", sc.pos), ("sw", sc.sw), ("alpha", sc.alpha), ("desc", sc.desc))}
     nf = rasts[0].grad_floats(sc.n)
     ref = torch.zeros(nf, device=dev)
-    step({k: v.to(dev) for k, v in host.items()}, ref)
+    tdist.cuda_batch_step(rasts, cams, dv["pos"], dv["sw"], dv["alpha"], dv["desc"], G, range(3), ref)
     torch.cuda.synchronize()
     ref = ref.cpu().numpy()
+
+    flat, n, F = tdist.flat_inputs(dv["pos"], dv["sw"], dv["alpha"], dv["desc"])
+    host_flat = flat.cpu().pin_memory()
+    pipe = tdist.ShardedStreamedSteps(host_flat, nf, dev)
+    assert pipe.h2d_bytes == host_flat.numel() * 4 and pipe.d2h_bytes == nf * 4
     out = [torch.zeros(nf).pin_memory() for _ in range(2)]
-    pipe = tdist.StreamedSteps(host, torch.zeros(nf, device=dev), dev)
+
+    def step(dev_flat, g, o):
+        pos, sw, al, de = tdist.input_views(dev_flat, n, F)
+        tdist.cuda_batch_step(rasts, cams, pos, sw, al, de, G, range(3), g, reduce="reduce_scatter", out=o)
+
     pipe.run(5, step, out)
     torch.cuda.synchronize()
     for o in out:

@@ -11,9 +11,13 @@ SRC = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), 
                    "csrc", "kernels.cuh")
 
 
-def network(n):
+def network(n, branch=0):
+    """Comparators of sort_small<n> as compiled; for a body with an #if/#else (TRIPS_NET16),
+    branch 0 is the default (#if) network and branch 1 the #else one."""
     src = open(SRC).read()
     body = src.split(f"sort_small<{n}>(uint64_t (&t)[16])\n{{", 1)[1].split("\n}", 1)[0]
+    if "#else" in body:
+        body = body.split("#else")[branch]
     return [(int(a), int(b)) for a, b in re.findall(r"cswap\(t\[(\d+)\], t\[(\d+)\]\)", body)]
 
 
@@ -29,18 +33,44 @@ def all_binary(n):
     return ((np.arange(1 << n)[:, None] >> np.arange(n)) & 1).astype(np.int8)
 
 
+def _sorts_all(net, n):
+    out = apply(net, all_binary(n))
+    return bool(np.all(np.diff(out, axis=1) >= 0))
+
+
+def test_sort4_network_sorts():
+    net = network(4)
+    assert len(net) == 5 and all(i < j < 4 for i, j in net)
+    assert _sorts_all(net, 4)
+
+
 def test_sort8_network_sorts():
     net = network(8)
     assert len(net) == 19 and all(i < j < 8 for i, j in net)
-    out = apply(net, all_binary(8))
-    assert np.all(np.diff(out, axis=1) >= 0)
+    assert _sorts_all(net, 8)
+
+
+def test_sort12_network_sorts():
+    net = network(12)
+    assert len(net) == 39 and all(i < j < 12 for i, j in net)
+    assert _sorts_all(net, 12)
 
 
 def test_sort16_network_sorts():
-    net = network(16)
-    assert len(net) == 63 and all(i < j < 16 for i, j in net)
-    out = apply(net, all_binary(16))
-    assert np.all(np.diff(out, axis=1) >= 0)
+    net = network(16)                    # default: 60 comparators
+    assert len(net) == 60 and all(i < j < 16 for i, j in net)
+    assert _sorts_all(net, 16)
+    batcher = network(16, branch=1)      # TRIPS_NET16 = 0
+    assert len(batcher) == 63 and all(i < j < 16 for i, j in batcher)
+    assert _sorts_all(batcher, 16)
+
+
+def test_networks_fail_when_a_comparator_is_dropped():
+    """The exhaustive check has teeth: every comparator of the 12- and 16-key networks is needed."""
+    for n in (12, 16):
+        net = network(n)
+        for k in range(len(net)):
+            assert not _sorts_all(net[:k] + net[k + 1:], n)
 
 
 def merge_keep16(r, t, n):
@@ -59,7 +89,7 @@ def merge_keep16(r, t, n):
 def test_merge_keeps_16_smallest_random():
     """Random distinct keys (the kernel's keys are unique): merge = sort(union)[:16]."""
     rng = np.random.default_rng(0)
-    for n in (8, 16):
+    for n in (4, 8, 12, 16):
         for _ in range(3000):
             keys = rng.permutation(1000)[:16 + n]
             r = np.sort(keys[:16])
@@ -71,12 +101,11 @@ def test_merge_keeps_16_smallest_random():
 
 def test_merge_zero_one_exhaustive_small():
     """0-1 principle on the merge for all sorted 0/1 inputs (r and t sorted: 17 x 17 cases)."""
-    for n in (8, 16):
+    for n in (4, 8, 12, 16):
         for a, b in itertools.product(range(17), range(n + 1)):
             r = np.array([0] * a + [1] * (16 - a))
             t = np.array([0] * b + [1] * (16 - b))
-            if n == 8:
-                t[8:] = 1
+            t[n:] = 1
             got = merge_keep16(r[None], t[None], n)[0]
             zeros = min(16, a + b)
             assert np.array_equal(got, np.array([0] * zeros + [1] * (16 - zeros)))

@@ -41,9 +41,10 @@ for v in range(args.views):
     r.forward(save=True)
 torch.cuda.synchronize()
 fn(buf, 1)
-names = ["A (fragments, ranks)", "scan", "B (scatter)", "C (sort/merge)", "kept-offset scan", "D (blend)",
-         "E (store)"]
-vals = np.array(list(buf)[:7], dtype=np.float64)
+names = ["A (fragments, ranks)", "scan", "B (scatter)", "C (sort/merge)", "kept keys to smem", "D (blend)",
+         "E (store)", "F (kept pairs)"]
+vals = np.array(list(buf)[:8], dtype=np.float64)
 tot = vals.sum()
+print(os.environ.get("TRIPS_LIB", "in-tree"), f"total {tot:.4g} CTA-cycles")
 for n, v in zip(names, vals):
     print(f"{n:22s} {100 * v / tot:5.1f}%")
