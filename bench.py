@@ -54,6 +54,15 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def measured_peaks():
+    """MEASURED_PEAKS.json as a dict (empty when absent)."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
 def host_info():
     model = None
     try:
@@ -487,6 +496,37 @@ def run_cuda(args, rank, world, local_rank):
     torch.cuda.synchronize()
     knn_ms = k0.elapsed_time(k1) / 3
 
+    # ---- side measurement: the gated-conv decoder on this bench's pyramid
+    # geometry (1080p, 4 layers, F = 4 -> 3 channels), tcgen05 implicit-GEMM convolutions
+    from paper_2401_06003_b200 import Decoder
+    dec = Decoder(rast, 3)
+    gen = torch.Generator(device=dev).manual_seed(3)
+    dec_prm = (torch.randn(dec.param_count, generator=gen, device=dev) * 0.1).contiguous()
+    dec_pyr = (torch.randn(rast.pyramid_floats, generator=gen, device=dev) * 0.5).contiguous()
+    dec_out = dec(dec_prm, dec_pyr)
+    torch.cuda.synchronize()
+    k0.record(stream)
+    for _ in range(10):
+        dec(dec_prm, dec_pyr, dec_out)
+    k1.record(stream)
+    torch.cuda.synchronize()
+    dec_ms = k0.elapsed_time(k1) / 10
+    dec_flops = 2.0 * H * W * 32 * 3                     # output projection
+    for l in range(sc.n_layers):
+        hl, wl, _ = _abi.trips_layer_dims(rast.plan, l)
+        C = F + 1 if l == sc.n_layers - 1 else 32 + F + 1
+        dec_flops += 2.0 * hl * wl * (2 * 32 * C * 9 + 32 * C)   # Wf, Wg (3x3) and Wb (1x1)
+    tc_peak = measured_peaks().get("bf16_tflops")
+    decoder = {"workload": f"{W}x{H}, {sc.n_layers} layers, F={F} -> 3 channels (fp16 operands, fp32 accumulate)",
+               "ms_per_frame": dec_ms, "frames_per_s": 1e3 / dec_ms,
+               "alg_tflops": dec_flops / (dec_ms * 1e-3) / 1e12, "alg_flops_per_frame": dec_flops,
+               "bound": "tensor", "peak_tflops": tc_peak,
+               "peak_source": "MEASURED_PEAKS.json bf16_tflops (fp16 runs at the bf16 rate)" if tc_peak else None}
+    if tc_peak:
+        decoder["frac"] = decoder["alg_tflops"] / tc_peak
+    del dec, dec_prm, dec_pyr, dec_out
+    torch.cuda.empty_cache()
+
     # ---- end to end through the public API: pinned host inputs in, gradients out.  Each rank
     # uploads its 1/N slice of the flat input buffer (+ NCCL all-gather) and downloads its 1/N
     # shard of the reduce-scattered gradients (dist.ShardedStreamedSteps; at N = 1 the whole
@@ -593,6 +633,7 @@ def run_cuda(args, rank, world, local_rank):
     line["backward_ms_per_view"] = cam_ms
     line["variants_ms_per_view"] = variants
     line["knn4_size_init"] = {"ms": knn_ms, "points_per_s": n / (knn_ms * 1e-3)}
+    line["decoder"] = decoder
     if configs:
         line["configs"] = configs
     if world == 1 and not args.no_cpu_baseline:

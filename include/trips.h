@@ -242,6 +242,37 @@ int trips_morton_order(void* ws, int64_t n, const float* pos, int32_t* perm_out,
 size_t trips_knn_workspace_bytes(int64_t n);
 int trips_knn_sizes(void* ws, int64_t n, const float* pos, float* size_out, int32_t* nbr_out, void* stream);
 
+/* ---- decoder ---------------------------------------------------------------------- */
+
+/* The gated-convolution decoder over the pyramid (Sec.
+ * 3.3 and Fig. fig:conv: "a single gated convolution in each layer with a self-bypass connection
+ * and a feature size of 32 ... a bilinear upsampling operation for all layers except the final
+ * one, merging the output with the subsequent level"; readings D1-D8 in DESIGN.md):
+ *   for l = n-1 .. 0:  x_l = [U(y_{l+1}) cropped to the layer (32 ch, absent at l = n-1),
+ *                             pyramid layer l (F features + opacity)]
+ *                      y_l = ELU(conv3x3(x_l; Wf_l) + bf_l) * sigmoid(conv3x3(x_l; Wg_l) + bg_l)
+ *                            + Wb_l x_l                         (zero-padded 3x3 convolutions)
+ *   out = Wo y_0 + bo                                           (1x1, out_channels = 3 or 27)
+ * U = bilinear 2x upsampling with half-pixel centres, edge-clamped.  The 3x3 convolutions and
+ * the bypass run on the tcgen05 tensor cores with fp16 operands (x_l and the weights rounded to
+ * half) and fp32 accumulation; biases, activations and the output projection in fp32.
+ *   params  float[trips_decoder_param_count(plan, out_channels)] device, layer by layer
+ *           (l = 0 .. n-1): Wf [32][C_l][3][3], bf [32], Wg [32][C_l][3][3], bg [32], Wb [32][C_l]
+ *           with C_l = F + 1 for the coarsest layer, 32 + F + 1 otherwise (input channel order:
+ *           the 32 upsampled channels, then the pyramid's F features and its opacity); then
+ *           Wo [out_channels][32], bo [out_channels].  4-B aligned.
+ *   pyramid float[trips_pyramid_floats(plan)] device, the layout trips_splat_forward writes
+ *   out     float[out_channels][H][W] device (full resolution, planar)
+ *   dws     device scratch of trips_decoder_workspace_bytes(plan) bytes, 256-B aligned; holds
+ *           the packed fp16 weights and the per-layer activations (independent of the
+ *           rasterizer's workspace; the plan only supplies the pyramid geometry).
+ * Errors: TRIPS_ERR_ARG (null pointer, out_channels outside [1, 32], F + 1 > 32),
+ * TRIPS_ERR_ALIGN, TRIPS_ERR_CUDA (launch failure, no tensor-map encoder). */
+int64_t trips_decoder_param_count(const trips_plan* plan, int32_t out_channels);
+size_t trips_decoder_workspace_bytes(const trips_plan* plan);
+int trips_decode(const trips_plan* plan, void* dws, const float* params, int32_t out_channels,
+                 const float* pyramid, float* out, void* stream);
+
 /* ---- measurement ------------------------------------------------------------------ */
 
 /* Memory-operation microbenchmark giving the measured ceilings the backward's gradient

@@ -11,5 +11,6 @@ There is no CPU fallback: importing the binding loads libtrips.so or raises.
 """
 from . import _abi  # noqa: F401
 from .rasterizer import Rasterizer, knn_sizes, morton_order, render  # noqa: F401
+from .decoder import Decoder  # noqa: F401
 
-__all__ = ["Rasterizer", "render", "morton_order", "knn_sizes"]
+__all__ = ["Rasterizer", "render", "morton_order", "knn_sizes", "Decoder"]

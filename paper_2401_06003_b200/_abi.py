@@ -76,6 +76,9 @@ SIGNATURES = [
     ("trips_knn_sizes", C.c_int, [_VP, C.c_int64, _VP, _VP, _VP, _VP]),
     ("trips_microbench", C.c_int, [C.c_int32, C.c_int32, _VP, C.c_int64, C.c_int32, C.c_int64, _VP,
                                    C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
+    ("trips_decoder_param_count", C.c_int64, [_VP, C.c_int32]),
+    ("trips_decoder_workspace_bytes", C.c_size_t, [_VP]),
+    ("trips_decode", C.c_int, [_VP, _VP, _VP, C.c_int32, _VP, _VP, _VP]),
     ("trips_launch_count", C.c_int64, []),
     ("trips_status_string", C.c_char_p, [C.c_int]),
 ]
@@ -218,3 +221,18 @@ def trips_microbench(op, pattern, buf, nbytes, row_bytes, ops, stream=None):
 
 def trips_launch_count():
     return int(lib().trips_launch_count())
+
+
+def trips_decoder_param_count(plan, out_channels):
+    n = int(lib().trips_decoder_param_count(plan, out_channels))
+    if n < 0:
+        raise TripsError(TRIPS_ERR_ARG, "trips_decoder_param_count")
+    return n
+
+
+def trips_decoder_workspace_bytes(plan):
+    return int(lib().trips_decoder_workspace_bytes(plan))
+
+
+def trips_decode(plan, dws, params, out_channels, pyramid, out, stream):
+    check(lib().trips_decode(plan, dws, params, out_channels, pyramid, out, stream), "trips_decode")

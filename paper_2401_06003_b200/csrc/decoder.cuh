@@ -1,0 +1,378 @@
+// decoder.cuh -- the gated-convolution decoder over the image pyramid:
+// "a single gated convolution in each layer with a self-bypass connection and a feature size of
+// 32 ... a bilinear upsampling operation for all layers except the final one, merging the output
+// with the subsequent level" (Fig. fig:conv; readings D1-D8 in DESIGN.md).
+//
+// Per layer l (coarsest first), three steps on the GPU:
+//   k_dec_prep   X_l[y][x][64] fp16 (NHWC): channels 0-31 = bilinear 2x upsampling of y_{l+1}
+//                (half-pixel centres, edge-clamped, cropped), 32-32+F = the pyramid layer's F
+//                features + opacity, the rest 0 (memory-bound elementwise pass);
+//   k_dec_conv   the 3x3 gated convolution + 1x1 bypass as ONE implicit GEMM on the tcgen05
+//                tensor cores: D[128 pixels][96] += A_tap[128][64] . B_tap[96][64]^T over the 9
+//                taps, where A_tap is the row segment of X_l shifted by the tap (a TMA box of the
+//                3-D tensor map: out-of-image taps are zero-filled by the TMA unit = the conv's
+//                zero padding) and B_tap the packed weights [f (32) | g (32) | bypass (32, centre
+//                tap only)]; fp16 operands, fp32 accumulators in TMEM.  Epilogue straight from
+//                TMEM: y = ELU(f + bf) * sigmoid(g + bg) + bypass, stored fp32 NHWC -- or, at the
+//                finest layer, the 1x1 output projection Wo y + bo, stored planar [out][H][W];
+//   (k_dec_pack  once per call: the flat fp32 parameter vector -> the packed fp16 B operands.)
+//
+// k_dec_conv is warp-specialised and persistent (one CTA per SM): warp 0 issues the TMA loads of
+// the A taps into a 4-stage ring (mbarrier full/empty pairs), warp 1 issues the tcgen05.mma
+// (one elected lane, 4 x K16 per tap), warps 2-9 drain the accumulator (double-buffered in TMEM,
+// 2 x 96 columns; two warps per TMEM lane quarter, 16 hidden channels each) while the next tile's
+// MMAs run.  The B operands of all 9 taps (108 KB) stay
+// resident in shared memory for the whole launch.
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+namespace trips {
+
+constexpr int kDecHidden = 32;             // "a feature size of 32"
+constexpr int kDecXC = 64;                 // X channels: 32 upsampled + F + 1 pyramid, zero-padded
+constexpr int kDecN = 96;                  // GEMM N: f (32) | g (32) | bypass (32)
+constexpr int kDecM = 128;                 // pixels per tile (one UMMA M)
+constexpr int kDecTaps = 9;
+constexpr int kDecStages = 4;
+constexpr int kDecABytes = kDecM * kDecXC * 2;          // 16 KB per tap
+constexpr int kDecBBytes = kDecN * kDecXC * 2;          // 12 KB per tap
+constexpr int kDecEpiWarps = 8;                         // 2 per TMEM lane quarter (16 channels each)
+constexpr int kDecThreads = 64 + 32 * kDecEpiWarps;     // TMA warp, MMA warp, epilogue warps
+constexpr int kDecMaxOut = 32;
+constexpr int kDecProjBytes = 4 * 32 * kDecMaxOut * 4;  // final layer: partial projections of the upper halves
+constexpr int kDecSmem = 1024 + kDecTaps * kDecBBytes + kDecStages * kDecABytes + kDecProjBytes + 256;
+
+// ----------------------------------------------------------------------------- PTX wrappers
+
+__device__ __forceinline__ uint32_t dec_smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void dec_mbar_init(uint64_t* bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(dec_smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void dec_mbar_expect_tx(uint64_t* bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(dec_smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void dec_mbar_arrive(uint64_t* bar)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(dec_smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void dec_mbar_wait(uint64_t* bar, uint32_t parity)
+{
+    asm volatile("{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+                 "@!P1 bra WAIT_%=;\n\t}" :: "r"(dec_smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void dec_tma_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2)
+{
+    asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
+                 :: "r"(dec_smem_u32(dst)), "l"(map), "r"(dec_smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2) : "memory");
+}
+__device__ __forceinline__ void dec_tma_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1)
+{
+    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+                 :: "r"(dec_smem_u32(dst)), "l"(map), "r"(dec_smem_u32(bar)), "r"(c0), "r"(c1) : "memory");
+}
+__device__ __forceinline__ void dec_tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void dec_tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// K-major operand in the canonical 128-byte-swizzled layout (8-row groups of 128-byte rows,
+// 1024 B apart; the TMA box writes exactly this): start >> 4, LBO = 1 (unused for swizzled
+// K-major), SBO = 1024 B >> 4, version 1 (sm_100), layout SWIZZLE_128B (2).
+__device__ __forceinline__ uint64_t dec_desc(uint32_t saddr)
+{
+    return (uint64_t)((saddr >> 4) & 0x3fffu) | (1ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
+}
+// instruction descriptor, kind::f16: D f32 (bits 4-5 = 1), A = B = f16 (0), both K-major,
+// N >> 3 at bits 17-22, M >> 4 at bits 24-28
+constexpr uint32_t kDecIdesc = (1u << 4) | ((uint32_t)(kDecN >> 3) << 17) | ((uint32_t)(kDecM >> 4) << 24);
+
+__device__ __forceinline__ void dec_umma(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accumulate)
+{
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                 "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+                 :: "r"(d_tmem), "l"(a), "l"(b), "r"(kDecIdesc), "r"(accumulate));
+}
+__device__ __forceinline__ void dec_umma_commit(uint64_t* bar)
+{
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                 :: "r"(dec_smem_u32(bar)) : "memory");
+}
+// 32 lanes x 16 consecutive fp32 columns: thread t of the warp gets lane (base + t), columns c..c+15
+// (no wait: the caller issues tcgen05.wait::ld once after all its loads)
+__device__ __forceinline__ void dec_tmem_ld16(uint32_t taddr, uint32_t (&r)[16])
+{
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+                 "%14, %15}, [%16];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                   "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+                 : "r"(taddr));
+}
+__device__ __forceinline__ void dec_tmem_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void dec_bar_pair(int id) { asm volatile("bar.sync %0, 64;" :: "r"(id) : "memory"); }
+
+// ----------------------------------------------------------------------------- parameters
+
+struct DecLayer {
+    int32_t H, W;                  // layer size
+    int32_t Hc, Wc;                // next-coarser layer size (0 at the coarsest)
+    int64_t pyr_off;               // float offset of the layer in the planar pyramid
+    int64_t prm_off;               // float offset of the layer's block in the flat parameters
+    int32_t C;                     // input channels of the block (F + 1 coarsest, 32 + F + 1 else)
+    int32_t coarsest;
+};
+
+struct DecParams {
+    int32_t n_layers, F, out_ch;
+    DecLayer L[16];
+    int64_t prm_out;               // float offset of Wo [out][32], bo [out]
+    const float* prm;              // flat fp32 parameters (oracle/decoder.py param_layout)
+    const float* pyramid;          // the rasterizer's planar pyramid
+    __half* wpack;                 // [n][9][96][64] packed B operands
+    __half* X;                     // [H_l][W_l][64] current layer input
+    float* Y[2];                   // [H_l][W_l][32] hidden outputs (ping-pong by layer parity)
+    float* out;                    // [out][H][W]
+};
+
+// k_dec_pack: B[l][t][n][k] = Wf / Wg (3x3 tap t = (dy+1)*3 + (dx+1)) or Wb (centre tap), with
+// the block's input channel c at X channel k = c (32 + c at the coarsest layer: no upsampled part).
+__global__ void __launch_bounds__(256) k_dec_pack(DecParams D)
+{
+    const int64_t total = (int64_t)D.n_layers * kDecTaps * kDecN * kDecXC;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int k = (int)(e % kDecXC);
+        const int n = (int)((e / kDecXC) % kDecN);
+        const int t = (int)((e / (kDecXC * kDecN)) % kDecTaps);
+        const int l = (int)(e / ((int64_t)kDecXC * kDecN * kDecTaps));
+        const DecLayer& L = D.L[l];
+        const int c = L.coarsest ? k - kDecHidden : k;
+        float v = 0.f;
+        if (c >= 0 && c < L.C) {
+            const float* P = D.prm + L.prm_off;
+            const int64_t wsz = (int64_t)kDecHidden * L.C * 9;
+            if (n < 32) v = P[((int64_t)n * L.C + c) * 9 + t];                                   // Wf
+            else if (n < 64) v = P[wsz + kDecHidden + ((int64_t)(n - 32) * L.C + c) * 9 + t];    // Wg
+            else if (t == 4) v = P[2 * (wsz + kDecHidden) + (int64_t)(n - 64) * L.C + c];       // Wb
+        }
+        D.wpack[e] = __float2half_rn(v);
+    }
+}
+
+// k_dec_prep: X_l (see the header).  One thread per (pixel, 8-channel group): 16-byte stores.
+__global__ void __launch_bounds__(256) k_dec_prep(DecParams D, int l)
+{
+    const DecLayer& L = D.L[l];
+    const int npx = L.H * L.W;                       // < 2^31 / 8 (checked on the host)
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= npx * (kDecXC / 8)) return;
+    const int grp = e & (kDecXC / 8 - 1);
+    const int p = e >> 3;
+    const int y = p / L.W, x = p - y * L.W;
+    float v[8];
+    if (grp < kDecHidden / 8) {
+        if (L.coarsest) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[j] = 0.f;
+        } else {
+            // bilinear 2x, half-pixel centres: output i samples (i + 0.5) / 2 - 0.5 >= 0 (clamped)
+            const float* Yc = D.Y[(l + 1) & 1];
+            const float sy = fmaxf((y + 0.5f) * 0.5f - 0.5f, 0.f), sx = fmaxf((x + 0.5f) * 0.5f - 0.5f, 0.f);
+            const int y0 = min((int)sy, L.Hc - 1), x0 = min((int)sx, L.Wc - 1);
+            const int y1 = min(y0 + 1, L.Hc - 1), x1 = min(x0 + 1, L.Wc - 1);
+            const float ly = sy - (float)y0, lx = sx - (float)x0;
+            const float4* a = reinterpret_cast<const float4*>(Yc + ((int64_t)y0 * L.Wc + x0) * kDecHidden + grp * 8);
+            const float4* b = reinterpret_cast<const float4*>(Yc + ((int64_t)y0 * L.Wc + x1) * kDecHidden + grp * 8);
+            const float4* c = reinterpret_cast<const float4*>(Yc + ((int64_t)y1 * L.Wc + x0) * kDecHidden + grp * 8);
+            const float4* d = reinterpret_cast<const float4*>(Yc + ((int64_t)y1 * L.Wc + x1) * kDecHidden + grp * 8);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const float4 A = a[h], B = b[h], C = c[h], Dd = d[h];
+                const float r0[4] = {A.x, A.y, A.z, A.w}, r1[4] = {B.x, B.y, B.z, B.w};
+                const float r2[4] = {C.x, C.y, C.z, C.w}, r3[4] = {Dd.x, Dd.y, Dd.z, Dd.w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const float top = r0[j] * (1.f - lx) + r1[j] * lx;
+                    const float bot = r2[j] * (1.f - lx) + r3[j] * lx;
+                    v[4 * h + j] = top * (1.f - ly) + bot * ly;
+                }
+            }
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int ch = (grp * 8 + j) - kDecHidden;
+            v[j] = ch <= D.F ? __ldg(D.pyramid + L.pyr_off + (int64_t)ch * npx + p) : 0.f;
+        }
+    }
+    __half2 h2[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) h2[j] = __floats2half2_rn(v[2 * j], v[2 * j + 1]);
+    *reinterpret_cast<uint4*>(D.X + (int64_t)p * kDecXC + grp * 8) = *reinterpret_cast<uint4*>(h2);
+}
+
+// fast-math activations (ex2.approx based): |error| ~ 1e-7 absolute, far inside the fp16-operand
+// tolerance of the decoder (D8)
+__device__ __forceinline__ float dec_elu(float v) { return v > 0.f ? v : __expf(v) - 1.f; }
+__device__ __forceinline__ float dec_sigmoid(float v) { return __fdividef(1.f, 1.f + __expf(-v)); }
+
+// k_dec_conv: see the header.  tmX: 3-D map of X_l {64 ch, W, H}, box {64, 128, 1}, SWIZZLE_128B;
+// tmB: 2-D map of the packed weights {64, n * 9 * 96}, box {64, 96}, SWIZZLE_128B.
+__global__ void __launch_bounds__(kDecThreads, 1) k_dec_conv(const __grid_constant__ CUtensorMap tmX,
+                                                            const __grid_constant__ CUtensorMap tmB, DecParams D, int l)
+{
+    extern __shared__ __align__(1024) uint8_t dec_smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dec_smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sB = smem;                                           // 9 x 12 KB
+    uint8_t* sA = smem + kDecTaps * kDecBBytes;                   // stages x 16 KB
+    float* sProj = reinterpret_cast<float*>(sA + kDecStages * kDecABytes);   // [4][32][out]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sA + kDecStages * kDecABytes + kDecProjBytes);
+    uint64_t* full = bars;                                        // [stages]
+    uint64_t* empty = bars + kDecStages;                          // [stages]
+    uint64_t* tfull = bars + 2 * kDecStages;                      // [2]
+    uint64_t* tempty = tfull + 2;                                 // [2]
+    uint64_t* bbar = tempty + 2;                                  // weights loaded
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bbar + 1);
+
+    const DecLayer& L = D.L[l];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int xt = (L.W + kDecM - 1) / kDecM;
+    const int ntiles = L.H * xt;
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < kDecStages; ++s) { dec_mbar_init(full + s, 1); dec_mbar_init(empty + s, 1); }
+        for (int a = 0; a < 2; ++a) { dec_mbar_init(tfull + a, 1); dec_mbar_init(tempty + a, kDecEpiWarps); }
+        dec_mbar_init(bbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {      // TMEM: 2 accumulators x 96 columns (256 allocated)
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                     :: "r"(dec_smem_u32(tmem_slot)), "n"(256) : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    dec_tc_fence_before();
+    __syncthreads();
+    dec_tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ---- TMA producer: the weights once, then the 9 shifted A boxes of every tile
+            dec_mbar_expect_tx(bbar, kDecTaps * kDecBBytes);
+            for (int t = 0; t < kDecTaps; ++t) dec_tma_2d(sB + t * kDecBBytes, &tmB, bbar, 0, (l * kDecTaps + t) * kDecN);
+            int s = 0;
+            uint32_t ph = 0;
+            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                const int y = tile / xt, x0 = (tile % xt) * kDecM;
+                for (int t = 0; t < kDecTaps; ++t) {
+                    dec_mbar_wait(empty + s, ph ^ 1);
+                    dec_mbar_expect_tx(full + s, kDecABytes);
+                    dec_tma_3d(sA + s * kDecABytes, &tmX, full + s, 0, x0 + (t % 3) - 1, y + (t / 3) - 1);
+                    if (++s == kDecStages) { s = 0; ph ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ---- MMA issuer
+            dec_mbar_wait(bbar, 0);
+            int s = 0;
+            uint32_t ph = 0;
+            int it = 0;
+            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+                const int acc = it & 1;
+                const uint32_t aph = (uint32_t)(it >> 1) & 1u;
+                dec_mbar_wait(tempty + acc, aph ^ 1);
+                dec_tc_fence_after();
+                const uint32_t d = tmem + (uint32_t)(acc * kDecN);
+                for (int t = 0; t < kDecTaps; ++t) {
+                    dec_mbar_wait(full + s, ph);
+                    dec_tc_fence_after();
+                    const uint32_t a0 = dec_smem_u32(sA + s * kDecABytes), b0 = dec_smem_u32(sB + t * kDecBBytes);
+#pragma unroll
+                    for (int k = 0; k < kDecXC / 16; ++k)    // K16 steps: +32 B inside the swizzle atom
+                        dec_umma(d, dec_desc(a0 + 32 * k), dec_desc(b0 + 32 * k), (t | k) ? 1u : 0u);
+                    dec_umma_commit(empty + s);               // smem slot free once these MMAs finish
+                    if (++s == kDecStages) { s = 0; ph ^= 1; }
+                }
+                dec_umma_commit(tfull + acc);                 // accumulator ready for the epilogue
+            }
+        }
+    } else {
+        // ---- epilogue warps 2-9: TMEM lane quarter q = warp % 4 (tile rows 32 q ..), channel half
+        // h (16 of the 32 hidden channels: f, g and bypass columns 16 h ..)
+        const int q = warp & 3, h = (warp - 2) >> 2;
+        const float* P = D.prm + L.prm_off;
+        const int64_t wsz = (int64_t)kDecHidden * L.C * 9;
+        const float* bf = P + wsz + 16 * h;
+        const float* bg = P + 2 * wsz + kDecHidden + 16 * h;
+        const bool last = l == 0;
+        float* Yo = D.Y[l & 1];
+        float* proj = sProj + (q * 32 + lane) * kDecMaxOut;
+        int it = 0;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+            const int acc = it & 1;
+            const uint32_t aph = (uint32_t)(it >> 1) & 1u;
+            dec_mbar_wait(tfull + acc, aph);
+            dec_tc_fence_after();
+            const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * kDecN + 16 * h);
+            uint32_t f[16], g[16], b[16];
+            dec_tmem_ld16(ta, f);
+            dec_tmem_ld16(ta + 32, g);
+            dec_tmem_ld16(ta + 64, b);
+            dec_tmem_wait();
+            dec_tc_fence_before();
+            __syncwarp();
+            if (lane == 0) dec_mbar_arrive(tempty + acc);    // TMEM buffer may be refilled
+            const int y = tile / xt, x = (tile % xt) * kDecM + 32 * q + lane;
+            float o[16];
+#pragma unroll
+            for (int c = 0; c < 16; ++c)
+                o[c] = dec_elu(__uint_as_float(f[c]) + __ldg(bf + c)) * dec_sigmoid(__uint_as_float(g[c]) + __ldg(bg + c)) +
+                       __uint_as_float(b[c]);
+            const int64_t p = (int64_t)y * L.W + x;
+            if (!last) {
+                if (x < L.W) {
+                    float4* dst = reinterpret_cast<float4*>(Yo + p * kDecHidden + 16 * h);
+#pragma unroll
+                    for (int c4 = 0; c4 < 4; ++c4) dst[c4] = make_float4(o[4 * c4], o[4 * c4 + 1], o[4 * c4 + 2], o[4 * c4 + 3]);
+                }
+            } else {
+                // output projection Wo y + bo: each half projects its 16 channels; the upper half
+                // hands its partial sums to the lower half through shared memory (64-thread barrier
+                // of the warp pair)
+                const float* Wo = D.prm + D.prm_out + 16 * h;
+                const float* bo = D.prm + D.prm_out + (int64_t)D.out_ch * kDecHidden;
+                const int64_t plane = (int64_t)L.H * L.W;
+                if (h == 1) {
+                    for (int oc = 0; oc < D.out_ch; ++oc) {
+                        float sacc = 0.f;
+#pragma unroll
+                        for (int c = 0; c < 16; ++c) sacc = fmaf(__ldg(Wo + oc * kDecHidden + c), o[c], sacc);
+                        proj[oc] = sacc;
+                    }
+                }
+                dec_bar_pair(1 + q);
+                if (h == 0) {
+                    for (int oc = 0; oc < D.out_ch; ++oc) {
+                        float sacc = __ldg(bo + oc) + proj[oc];
+#pragma unroll
+                        for (int c = 0; c < 16; ++c) sacc = fmaf(__ldg(Wo + oc * kDecHidden + c), o[c], sacc);
+                        if (x < L.W) D.out[oc * plane + p] = sacc;
+                    }
+                }
+                dec_bar_pair(1 + q);                         // proj may be rewritten for the next tile
+            }
+        }
+    }
+    __syncthreads();
+    if (warp == 1) {
+        dec_tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "n"(256) : "memory");
+    }
+}
+
+}  // namespace trips

@@ -2,220 +2,120 @@
 // ("Point sizes are initialized with the average distance to the four nearest
 // neighbor"; reading Q25 in DESIGN.md).
 //
-// Uniform grid over the cloud's bounding box (about one point per cell), points bucketed per
-// cell (count, scan, fill), then one thread per point searches cells ring by ring around its
-// own cell with a register top-4 of (d^2, j) and stops once every point outside the scanned
-// cube is provably farther than its 4th neighbour.  d^2 and the mean use the pinned fp32
-// sequence of the definition, so results are bit-identical to a brute-force evaluation.
+// Exact k-NN on a Morton-sorted cloud, sized by the data rather than by the bounding box (the
+// uniform grid of round 1 assumed volumetric density: on a surface cloud its cells held hundreds
+// of points and a query scanned thousands):
+//   1. 45-bit Morton codes of the points quantised to 2^15 steps per axis over the bounding cube
+//      (non-finite points get a code above every finite one), stable LSD radix sort (6 x 8 bits,
+//      morton.cuh's kernels), points gathered into sorted order;
+//   2. one thread per sorted position (so a warp's queries are spatial neighbours): a register
+//      top-4 of (d^2, j) over the +-kKnnWin neighbours in sorted order gives an upper bound r on
+//      the 4th distance; the box of half-width r (widened for rounding) around the point is a
+//      Z-order range query on the sorted codes: scan [code(box min), code(box max)] from a
+//      galloping lower_bound, test each code's axis bits against the box, and jump over the
+//      stretches of the curve outside it with BIGMIN (Tropf & Herzog) + lower_bound (window
+//      positions skipped: already considered).
+// Every point j with (d^2, j) below the window's 4th key lies in the box, so the top-4 is exact;
+// d^2 and the mean use the pinned fp32 sequence of the definition, so results are bit-identical
+// to a brute-force evaluation (tests/test_gpu_knn.py).
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "morton.cuh"
+
 namespace trips {
 
-struct KnnGrid {
-    float lo[3];
-    float h, inv_h;
-    int dim[3];
-    int ncell;
-};
+constexpr int kKnnBits = 15;                  // quantisation steps per axis: 2^15
+constexpr int kKnnPasses = 6;                 // 45-bit codes + the non-finite marker's bit 47
+constexpr uint64_t kKnnNonFinite = (1ull << 48) - 1;
+constexpr int kKnnWin = 8;                    // sorted-order neighbours on each side for the bound
 
 struct KnnWs {
-    int n, cap;               // points, cell capacity (>= ncell)
-    uint32_t* bbox;           // [6] orderable float bits (min xyz, max xyz)
-    KnnGrid* grid;            // [1]
-    uint32_t* cell_of;        // [n]  cell of each point (0xffffffff: not finite)
-    uint32_t* cnt;            // [cap + 1] counts -> exclusive offsets
-    uint32_t* cur;            // [cap]  fill cursors
-    uint32_t* bsum;           // [blocks] scan partials
-    float4* pts;              // [n]  (x, y, z, index bits) in cell order
+    using Key = uint64_t;
+    uint64_t* keys[2];        // [n] codes (sorted into keys[0] after the even number of passes)
+    uint32_t* vals[2];        // [n] point index (sorted into vals[0])
+    uint32_t* hist;           // [256][nblk]
+    uint32_t* bbox;           // [6] orderable float bits (min xyz, max xyz) of the finite points
+    uint32_t* nfin;           // [1] finite points (they sort first)
+    float4* pts;              // [n] (x, y, z, index bits) in sorted order
+    int n, nblk, last_pass;
 };
 
-__device__ __forceinline__ uint32_t knn_f2ord(float f)
+#ifdef TRIPS_KNN_STATS    // experiment builds only: candidates, lower_bound steps, BIGMIN jumps, boxes
+__device__ unsigned long long g_knn_stats[4];
+#define TRIPS_KNN_COUNT(k, v) atomicAdd(&g_knn_stats[k], (unsigned long long)(v))
+#else
+#define TRIPS_KNN_COUNT(k, v) (void)0
+#endif
+
+struct KnnQuant {
+    double lo[3];
+    double scale;             // steps per unit (0 for a single-point extent)
+};
+
+__device__ __forceinline__ KnnQuant knn_quant(const uint32_t* bbox)
 {
-    const uint32_t b = __float_as_uint(f);
-    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+    KnnQuant Q;
+    double ext = 0.0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const bool any = bbox[a] != 0xffffffffu;
+        Q.lo[a] = any ? (double)ord2f(bbox[a]) : 0.0;
+        const double hi = any ? (double)ord2f(bbox[3 + a]) : 0.0;
+        ext = fmax(ext, hi - Q.lo[a]);
+    }
+    Q.scale = ext > 0.0 ? (double)(1 << kKnnBits) / ext : 0.0;
+    return Q;
 }
-__device__ __forceinline__ float knn_ord2f(uint32_t o)
+
+// quantised coordinate, clamped to [0, 2^kKnnBits - 1] (monotone in v)
+__device__ __forceinline__ int knn_q(double v, double lo, double scale)
 {
-    return __uint_as_float((o & 0x80000000u) ? (o & 0x7fffffffu) : ~o);
+    const double t = floor((v - lo) * scale);
+    return t < 0.0 ? 0 : (t > (double)((1 << kKnnBits) - 1) ? (1 << kKnnBits) - 1 : (int)t);
 }
+
+__device__ __forceinline__ uint64_t knn_spread(uint32_t v)
+{
+    uint64_t x = v & 0x1fffffu;
+    x = (x | x << 32) & 0x1f00000000ffffull;
+    x = (x | x << 16) & 0x1f0000ff0000ffull;
+    x = (x | x << 8) & 0x100f00f00f00f00full;
+    x = (x | x << 4) & 0x10c30c30c30c30c3ull;
+    x = (x | x << 2) & 0x1249249249249249ull;
+    return x;
+}
+
+__device__ __forceinline__ uint64_t knn_code(int qx, int qy, int qz)
+{
+    return knn_spread((uint32_t)qx) | (knn_spread((uint32_t)qy) << 1) | (knn_spread((uint32_t)qz) << 2);
+}
+
 __device__ __forceinline__ bool finite3(float x, float y, float z) { return isfinite(x) && isfinite(y) && isfinite(z); }
 
-__global__ void __launch_bounds__(256) k_knn_bbox(KnnWs W, const float* __restrict__ pos)
+__global__ void __launch_bounds__(256) k_knn_codes(KnnWs W, const float* __restrict__ pos)
 {
-    uint32_t lo[3] = {0xffffffffu, 0xffffffffu, 0xffffffffu}, hi[3] = {0u, 0u, 0u};
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < W.n; i += gridDim.x * blockDim.x) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const KnnQuant Q = knn_quant(W.bbox);
+    bool fin = false;
+    if (i < W.n) {
         const float x = pos[3 * (size_t)i], y = pos[3 * (size_t)i + 1], z = pos[3 * (size_t)i + 2];
-        if (!finite3(x, y, z)) continue;
-        const float p[3] = {x, y, z};
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            lo[a] = min(lo[a], knn_f2ord(p[a]));
-            hi[a] = max(hi[a], knn_f2ord(p[a]));
-        }
+        fin = finite3(x, y, z);
+        W.keys[0][i] = fin ? knn_code(knn_q(x, Q.lo[0], Q.scale), knn_q(y, Q.lo[1], Q.scale), knn_q(z, Q.lo[2], Q.scale))
+                           : kKnnNonFinite;
+        W.vals[0][i] = (uint32_t)i;
     }
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        lo[a] = __reduce_min_sync(0xffffffffu, lo[a]);
-        hi[a] = __reduce_max_sync(0xffffffffu, hi[a]);
-    }
-    if ((threadIdx.x & 31) == 0)
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            atomicMin(&W.bbox[a], lo[a]);
-            atomicMax(&W.bbox[3 + a], hi[a]);
-        }
+    const uint32_t c = __reduce_add_sync(0xffffffffu, fin ? 1u : 0u);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(W.nfin, c);
 }
 
-// one thread: grid of about one point per cell, at most `cap` cells, at most 2048 per axis
-__global__ void k_knn_setup(KnnWs W)
+__global__ void __launch_bounds__(256) k_knn_gather(KnnWs W, const float* __restrict__ pos)
 {
-    KnnGrid g;
-    double ext[3], vol = 1.0, emax = 0.0;
-    for (int a = 0; a < 3; ++a) {
-        const float lo = W.bbox[a] == 0xffffffffu ? 0.f : knn_ord2f(W.bbox[a]);
-        const float hi = W.bbox[a] == 0xffffffffu ? 0.f : knn_ord2f(W.bbox[3 + a]);
-        g.lo[a] = lo;
-        ext[a] = (double)hi - (double)lo;
-        emax = fmax(emax, ext[a]);
-    }
-    for (int a = 0; a < 3; ++a) vol *= fmax(ext[a], emax * 1e-3 + 1e-30);
-    double h = cbrt(vol / fmax((double)W.n, 1.0));
-    h = fmax(h, emax / 2048.0);
-    h = fmax(h, 1e-30);
-    for (int it = 0; it < 64; ++it) {
-        double cells = 1.0;
-        for (int a = 0; a < 3; ++a) {
-            g.dim[a] = (int)fmin(floor(ext[a] / h) + 1.0, 2048.0);
-            cells *= g.dim[a];
-        }
-        if (cells <= (double)W.cap) break;
-        h *= 1.26;
-    }
-    g.h = (float)h;
-    g.inv_h = (float)(1.0 / h);
-    g.ncell = g.dim[0] * g.dim[1] * g.dim[2];
-    *W.grid = g;
-}
-
-__device__ __forceinline__ int knn_cell_axis(float v, float lo, float inv_h, int dim)
-{
-    const int c = (int)floorf((v - lo) * inv_h);
-    return c < 0 ? 0 : (c >= dim ? dim - 1 : c);
-}
-
-__global__ void __launch_bounds__(256) k_knn_count(KnnWs W, const float* __restrict__ pos)
-{
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= W.n) return;
-    const KnnGrid g = *W.grid;
-    const float x = pos[3 * (size_t)i], y = pos[3 * (size_t)i + 1], z = pos[3 * (size_t)i + 2];
-    uint32_t c = 0xffffffffu;
-    if (finite3(x, y, z)) {
-        const int cx = knn_cell_axis(x, g.lo[0], g.inv_h, g.dim[0]);
-        const int cy = knn_cell_axis(y, g.lo[1], g.inv_h, g.dim[1]);
-        const int cz = knn_cell_axis(z, g.lo[2], g.inv_h, g.dim[2]);
-        c = (uint32_t)((cz * g.dim[1] + cy) * g.dim[0] + cx);
-        atomicAdd(&W.cnt[c], 1u);
-    }
-    W.cell_of[i] = c;
-}
-
-// two-level exclusive scan of cnt[0..ncell): per-block sums, then offsets
-__global__ void __launch_bounds__(1024) k_knn_scan_a(KnnWs W)
-{
-    __shared__ uint32_t ws[32];
-    const int ncell = W.grid->ncell;
-    const int e = blockIdx.x * 1024 + threadIdx.x;
-    uint32_t v = e < ncell ? W.cnt[e] : 0u;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = v;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        uint32_t s = 0;
-        for (int w = 0; w < 32; ++w) s += ws[w];
-        W.bsum[blockIdx.x] = s;
-    }
-}
-
-__global__ void __launch_bounds__(1024) k_knn_scan_b(KnnWs W)
-{
-    // one CTA: exclusive scan of the block sums (in place)
-    __shared__ uint32_t ws[32];
-    const int nb = (W.grid->ncell + 1023) / 1024;
-    uint32_t carry = 0;
-    for (int base = 0; base < nb; base += 1024) {
-        const int b = base + threadIdx.x;
-        const uint32_t v = b < nb ? W.bsum[b] : 0u;
-        uint32_t x = v;
-        const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= (unsigned)o) x += y;
-        }
-        if (lane == 31) ws[warp] = x;
-        __syncthreads();
-        if (warp == 0) {
-            uint32_t w = ws[lane];
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
-                if (lane >= (unsigned)o) w += y;
-            }
-            ws[lane] = w;
-        }
-        __syncthreads();
-        if (b < nb) W.bsum[b] = carry + (warp ? ws[warp - 1] : 0u) + x - v;
-        carry += ws[31];
-        __syncthreads();
-    }
-}
-
-__global__ void __launch_bounds__(1024) k_knn_scan_c(KnnWs W)
-{
-    __shared__ uint32_t ws[32];
-    const int ncell = W.grid->ncell;
-    const int e = blockIdx.x * 1024 + threadIdx.x;
-    const uint32_t v = e < ncell ? W.cnt[e] : 0u;
-    uint32_t x = v;
-    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= (unsigned)o) x += y;
-    }
-    if (lane == 31) ws[warp] = x;
-    __syncthreads();
-    if (warp == 0) {
-        uint32_t w = ws[lane];
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
-            if (lane >= (unsigned)o) w += y;
-        }
-        ws[lane] = w;
-    }
-    __syncthreads();
-    const uint32_t off = W.bsum[blockIdx.x] + (warp ? ws[warp - 1] : 0u) + x - v;
-    if (e < ncell) {
-        W.cnt[e] = off;
-        W.cur[e] = off;
-    }
-    if (e == ncell - 1) W.cnt[ncell] = off + v;
-}
-
-__global__ void __launch_bounds__(256) k_knn_fill(KnnWs W, const float* __restrict__ pos)
-{
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= W.n) return;
-    const uint32_t c = W.cell_of[i];
-    if (c == 0xffffffffu) return;
-    const uint32_t p = atomicAdd(&W.cur[c], 1u);
-    W.pts[p] = make_float4(pos[3 * (size_t)i], pos[3 * (size_t)i + 1], pos[3 * (size_t)i + 2],
-                           __uint_as_float((uint32_t)i));
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= W.n) return;
+    const uint32_t i = W.vals[0][k];
+    W.pts[k] = make_float4(pos[3 * (size_t)i], pos[3 * (size_t)i + 1], pos[3 * (size_t)i + 2], __uint_as_float(i));
 }
 
 // (d2, j) insertion into an ascending register top-4 (lexicographic; j breaks ties)
@@ -233,74 +133,153 @@ __device__ __forceinline__ void knn_insert(float (&bd)[4], uint32_t (&bj)[4], fl
     }
 }
 
-__global__ void __launch_bounds__(256) k_knn_query(KnnWs W, const float* __restrict__ pos, float* __restrict__ size_out,
-                                                   int32_t* __restrict__ nbr_out)
+// first position in [0, nf) whose code is >= c (codes sorted ascending), galloping from `hint`
+__device__ __forceinline__ int knn_lower_bound(const uint64_t* __restrict__ codes, int nf, uint64_t c, int hint)
 {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= W.n) return;
-    const KnnGrid g = *W.grid;
-    const uint32_t ci = W.cell_of[i];
+    int lo, hi;                                      // answer in (lo, hi]: codes[lo] < c <= codes[hi]
+    if (codes[hint] < c) {
+        lo = hint;
+        int step = 1;
+        for (;;) {
+            const int p = hint + step;
+            if (p >= nf) { hi = nf; break; }
+            if (codes[p] >= c) { hi = p; break; }
+            lo = p;
+            step <<= 1;
+        }
+    } else {
+        hi = hint;
+        int step = 1;
+        for (;;) {
+            const int p = hint - step;
+            if (p < 0) { lo = -1; break; }
+            if (codes[p] < c) { lo = p; break; }
+            hi = p;
+            step <<= 1;
+        }
+    }
+    while (hi - lo > 1) {
+        const int mid = lo + ((hi - lo) >> 1);
+        if (codes[mid] < c) lo = mid; else hi = mid;
+    }
+    return hi;
+}
+
+// Per-axis bits of interleaved codes: masking keeps each axis' order, so a code is inside the
+// box [zmin, zmax] (corner codes) iff every axis' masked bits lie between the corners' ones.
+constexpr uint64_t kKnnAxis = 0x1249249249249249ull;
+__device__ __forceinline__ bool knn_in_box(uint64_t c, uint64_t zmin, uint64_t zmax)
+{
+    bool in = true;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const uint64_t m = kKnnAxis << a;
+        in = in && (c & m) >= (zmin & m) && (c & m) <= (zmax & m);
+    }
+    return in;
+}
+
+// BIGMIN (Tropf & Herzog, 1981): the smallest code > c inside the box [zmin, zmax], for c inside
+// [zmin, zmax] as a number but outside the box; ~0 if there is none.  Walks the bits from the
+// top: where c, zmin and zmax disagree it either returns or narrows the box to the half that
+// can still hold codes above c ("load 1000" / "load 0111" on that axis' lower bits).
+__device__ __forceinline__ uint64_t knn_bigmin(uint64_t c, uint64_t zmin, uint64_t zmax)
+{
+    uint64_t big = ~0ull;
+    // above the highest bit where the corners differ, c, zmin and zmax agree (zmin <= c <= zmax):
+    // nothing to do there
+    for (int b = 63 - __clzll(zmin ^ zmax); b >= 0; --b) {
+        const uint64_t m = 1ull << b;
+        const uint64_t axis = kKnnAxis << (b % 3);
+        const uint64_t low = axis & (m - 1);             // this axis' bits below b
+        const uint64_t at = low | m;                     // ... and b itself
+        const int code = ((c & m) ? 4 : 0) | ((zmin & m) ? 2 : 0) | ((zmax & m) ? 1 : 0);
+        if (code == 1) {                                 // c 0, min 0, max 1
+            big = (zmin & ~at) | m;
+            zmax = (zmax & ~at) | low;
+        } else if (code == 3) {                          // c 0, min 1, max 1
+            return zmin;
+        } else if (code == 4) {                          // c 1, min 0, max 0
+            return big;
+        } else if (code == 5) {                          // c 1, min 0, max 1
+            zmin = (zmin & ~at) | m;
+        } else if (code == 2 || code == 6) {             // min > max on this axis: cannot happen
+            return big;
+        }
+    }
+    return big;
+}
+
+__global__ void __launch_bounds__(256) k_knn_query(KnnWs W, float* __restrict__ size_out, int32_t* __restrict__ nbr_out)
+{
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= W.n) return;
+    const int nf = (int)*W.nfin;
+    const uint64_t* __restrict__ codes = W.keys[0];
+    const float4* __restrict__ pts = W.pts;
+    const float4 p = pts[k];
+    const uint32_t i = __float_as_uint(p.w);
     float bd[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
     uint32_t bj[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};
     int nb = 0;
-    if (ci != 0xffffffffu) {
-        const float x = pos[3 * (size_t)i], y = pos[3 * (size_t)i + 1], z = pos[3 * (size_t)i + 2];
-        const int cx = (int)(ci % (uint32_t)g.dim[0]);
-        const int cy = (int)((ci / (uint32_t)g.dim[0]) % (uint32_t)g.dim[1]);
-        const int cz = (int)(ci / ((uint32_t)g.dim[0] * (uint32_t)g.dim[1]));
-        const int rmax = max(g.dim[0], max(g.dim[1], g.dim[2]));
-        for (int r = 0; r <= rmax; ++r) {
-            for (int dz = -r; dz <= r; ++dz) {
-                const int zz = cz + dz;
-                if (zz < 0 || zz >= g.dim[2]) continue;
-                for (int dy = -r; dy <= r; ++dy) {
-                    const int yy = cy + dy;
-                    if (yy < 0 || yy >= g.dim[1]) continue;
-                    const bool face = (dz == -r || dz == r || dy == -r || dy == r);
-                    for (int dx = -r; dx <= r; dx += (face || r == 0) ? 1 : 2 * r) {
-                        const int xx = cx + dx;
-                        if (xx < 0 || xx >= g.dim[0]) continue;
-                        const uint32_t c = (uint32_t)((zz * g.dim[1] + yy) * g.dim[0] + xx);
-                        const uint32_t b = W.cnt[c], e = W.cnt[c + 1];
-                        for (uint32_t k = b; k < e; ++k) {
-                            const float4 q = W.pts[k];
-                            const uint32_t j = __float_as_uint(q.w);
-                            if (j == (uint32_t)i) continue;
-                            const float ddx = __fsub_rn(q.x, x), ddy = __fsub_rn(q.y, y), ddz = __fsub_rn(q.z, z);
-                            float d2 = __fadd_rn(__fmul_rn(ddx, ddx), __fmul_rn(ddy, ddy));
-                            d2 = __fadd_rn(d2, __fmul_rn(ddz, ddz));
-                            ++nb;
-                            if (d2 < bd[3] || (d2 == bd[3] && j < bj[3])) knn_insert(bd, bj, d2, j);
-                        }
-                    }
+    auto cand = [&](int j) {
+        const float4 q = pts[j];
+        const float ddx = __fsub_rn(q.x, p.x), ddy = __fsub_rn(q.y, p.y), ddz = __fsub_rn(q.z, p.z);
+        float d2 = __fadd_rn(__fmul_rn(ddx, ddx), __fmul_rn(ddy, ddy));
+        d2 = __fadd_rn(d2, __fmul_rn(ddz, ddz));
+        const uint32_t jj = __float_as_uint(q.w);
+        ++nb;
+        TRIPS_KNN_COUNT(0, 1);
+        if (d2 < bd[3] || (d2 == bd[3] && jj < bj[3])) knn_insert(bd, bj, d2, jj);
+    };
+    if (k < nf) {
+        const int w0 = max(0, k - kKnnWin), w1 = min(nf - 1, k + kKnnWin);
+        for (int j = w0; j <= w1; ++j)
+            if (j != k) cand(j);
+        if (w0 > 0 || w1 < nf - 1) {
+            // the window holds >= kKnnWin >= 4 others, so bd[3] is finite: every point with a
+            // smaller (d^2, j) key lies within r of p (fp32 rounding of d^2 covered by the factor),
+            // hence inside the quantised box [qlo, qhi] (+-1 step for the quantisation rounding).
+            // Its points are the sorted positions whose code lies in [code(qlo), code(qhi)] AND
+            // whose per-axis bits lie in the box: scan that code range, jumping over the stretches
+            // of the curve outside the box with BIGMIN (the next code >= c inside the box).
+            const KnnQuant Q = knn_quant(W.bbox);
+            const double r = sqrt((double)bd[3]) * (1.0 + 1e-5);
+            const double pp[3] = {p.x, p.y, p.z};
+            int qlo[3], qhi[3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                qlo[a] = max(0, knn_q(pp[a] - r, Q.lo[a], Q.scale) - 1);
+                qhi[a] = min((1 << kKnnBits) - 1, knn_q(pp[a] + r, Q.lo[a], Q.scale) + 1);
+            }
+            const uint64_t zmin = knn_code(qlo[0], qlo[1], qlo[2]), zmax = knn_code(qhi[0], qhi[1], qhi[2]);
+            TRIPS_KNN_COUNT(3, 1);
+            TRIPS_KNN_COUNT(1, (uint64_t)(qhi[0] - qlo[0] + 1) * (uint64_t)(qhi[1] - qlo[1] + 1));
+            int j = knn_lower_bound(codes, nf, zmin, k);
+            while (j < nf) {
+                const uint64_t c = codes[j];
+                if (c > zmax) break;
+                if (knn_in_box(c, zmin, zmax)) {
+                    if (j < w0 || j > w1) cand(j);
+                    ++j;
+                } else {
+                    const uint64_t bm = knn_bigmin(c, zmin, zmax);
+                    TRIPS_KNN_COUNT(2, 1);
+                    if (bm == ~0ull) break;
+                    j = knn_lower_bound(codes, nf, bm, j);
                 }
             }
-            // every point outside the scanned cube is at least `gap` away
-            double gap = 1e300;
-            const int cc[3] = {cx, cy, cz};
-            const float pp[3] = {x, y, z};
-            bool covers_all = true;
-            for (int a = 0; a < 3; ++a) {
-                const double lo_face = (double)g.lo[a] + (double)(cc[a] - r) * g.h;
-                const double hi_face = (double)g.lo[a] + (double)(cc[a] + r + 1) * g.h;
-                if (cc[a] - r > 0) gap = fmin(gap, (double)pp[a] - lo_face);
-                if (cc[a] + r + 1 < g.dim[a]) gap = fmin(gap, hi_face - (double)pp[a]);
-                if (cc[a] - r > 0 || cc[a] + r + 1 < g.dim[a]) covers_all = false;
-            }
-            if (covers_all) break;
-            gap -= 1e-4 * g.h;                                 // cell-assignment rounding margin
-            if (nb >= 4 && gap > 0 && (double)bd[3] < gap * gap * (1.0 - 1e-5)) break;
         }
     }
     const int K = nb < 4 ? nb : 4;
-    float s = 0.f;
+    float sz = 0.f;
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
-        if (k < K) s = __fadd_rn(s, __fsqrt_rn(bd[k]));
-    size_out[i] = K ? __fdiv_rn(s, (float)K) : 0.f;
+    for (int m = 0; m < 4; ++m)
+        if (m < K) sz = __fadd_rn(sz, __fsqrt_rn(bd[m]));
+    size_out[i] = K ? __fdiv_rn(sz, (float)K) : 0.f;
     if (nbr_out)
 #pragma unroll
-        for (int k = 0; k < 4; ++k) nbr_out[4 * (size_t)i + k] = k < K ? (int32_t)bj[k] : -1;
+        for (int m = 0; m < 4; ++m) nbr_out[4 * (size_t)i + m] = m < K ? (int32_t)bj[m] : -1;
 }
 
 }  // namespace trips

@@ -116,39 +116,43 @@ __global__ void __launch_bounds__(256) k_sort_hist(WS W, int pass)
     W.hist[(size_t)threadIdx.x * W.nblk + blk] = h[threadIdx.x];
 }
 
-// One CTA: exclusive scan of the digit-major histogram (digit d, block b) in place.
+// One CTA: exclusive scan of the digit-major histogram (digit d, block b) in place.  Each thread
+// sums a contiguous run (the run's cache lines stay in L1 between the two passes), one block scan
+// of the 1024 run sums, then each thread rewrites its run as offsets: two passes over the array
+// instead of total / 1024 barrier-separated rounds.
 template <typename WS>
 __global__ void __launch_bounds__(1024) k_sort_scan(WS W)
 {
     __shared__ uint32_t ws[32];
     const int total = 256 * W.nblk;
-    uint32_t carry = 0;
-    for (int base = 0; base < total; base += 1024) {
-        const int e = base + threadIdx.x;
-        const uint32_t v = e < total ? W.hist[e] : 0u;
-        uint32_t x = v;
-        const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int per = (total + blockDim.x - 1) / blockDim.x;
+    const int e0 = min(total, (int)threadIdx.x * per), e1 = min(total, e0 + per);
+    uint32_t sum = 0;
+    for (int e = e0; e < e1; ++e) sum += W.hist[e];
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t x = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= (unsigned)o) x += y;
+    }
+    if (lane == 31) ws[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t w = ws[lane];
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= (unsigned)o) x += y;
+            const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= (unsigned)o) w += y;
         }
-        if (lane == 31) ws[warp] = x;
-        __syncthreads();
-        if (warp == 0) {
-            uint32_t w = ws[lane];
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
-                if (lane >= (unsigned)o) w += y;
-            }
-            ws[lane] = w;
-        }
-        __syncthreads();
-        const uint32_t pre = (warp ? ws[warp - 1] : 0u) + x - v;
-        if (e < total) W.hist[e] = carry + pre;
-        carry += ws[31];
-        __syncthreads();
+        ws[lane] = w;
+    }
+    __syncthreads();
+    uint32_t run = (warp ? ws[warp - 1] : 0u) + x - sum;
+    for (int e = e0; e < e1; ++e) {
+        const uint32_t v = W.hist[e];
+        W.hist[e] = run;
+        run += v;
     }
 }
 

@@ -15,6 +15,8 @@
 #include "knn.cuh"
 #include "morton.cuh"
 #include "microbench.cuh"
+#include "decoder.cuh"
+#include <cudaTypedefs.h>
 
 using namespace trips;
 
@@ -202,6 +204,13 @@ Params make_params(const trips_plan* p, void* ws)
 
 bool aligned(const void* ptr, size_t a) { return (reinterpret_cast<uintptr_t>(ptr) & (a - 1)) == 0; }
 
+#ifdef TRIPS_FC4_ONLY   // experiment builds (tools/ variants): F <= 4 only, ~6x faster to compile
+#define TRIPS_FC_SWITCH(FC, CALL)                \
+    switch (FC) {                                \
+    case 4: { constexpr int kFC = 4; CALL; } break;   \
+    default: return TRIPS_ERR_ARG;               \
+    }
+#else
 #define TRIPS_FC_SWITCH(FC, CALL)                \
     switch (FC) {                                \
     case 4: { constexpr int kFC = 4; CALL; } break;   \
@@ -214,6 +223,7 @@ bool aligned(const void* ptr, size_t a) { return (reinterpret_cast<uintptr_t>(pt
     case 32: { constexpr int kFC = 32; CALL; } break; \
     default: return TRIPS_ERR_ARG;               \
     }
+#endif
 
 }  // namespace
 
@@ -264,7 +274,7 @@ int trips_plan_create(const trips_config* cfg, int32_t width, int32_t height, in
     p->off_hist = o;   o = align256(o + (size_t)p->ctas * tiles * 4);
     p->off_cvis = o;   o = align256(o + (size_t)p->ctas * 4);
     p->off_toff = o;   o = align256(o + ((size_t)tiles + 1) * 4);
-    p->off_tcnt = o;   o = align256(o + (size_t)tiles * 4);
+    p->off_tcnt = o;   o = align256(o + (size_t)(tiles + 1) * 4);   // [T] = k_count completion ticket
     p->off_bkey = o;   o = align256(o + 8 * N * 8);
     p->off_borig = o;  o = align256(o + 8 * N * 2);
     p->off_pcnt = o;  o = align256(o + (size_t)tiles * kTilePix * 4);
@@ -337,7 +347,7 @@ int trips_project(trips_plan* p, void* ws, const trips_camera* c, int64_t n, con
     P.pos = pos; P.sw = world_size; P.alpha = opacity; P.desc = desc;
     int rc = cuda_status(cudaMemsetAsync(P.stats, 0, S_COUNT * 8, st));
     if (rc) return rc;
-    rc = cuda_status(cudaMemsetAsync(P.tile_cnt, 0, (size_t)p->T * 4, st));
+    rc = cuda_status(cudaMemsetAsync(P.tile_cnt, 0, (size_t)(p->T + 1) * 4, st));
     if (rc) return rc;
     const size_t hsm = (size_t)p->T * 4;
     if ((rc = set_smem_attrs(hsm))) return rc;
@@ -346,7 +356,7 @@ int trips_project(trips_plan* p, void* ws, const trips_camera* c, int64_t n, con
         TRIPS_FC_SWITCH(p->FC, (k_count<kFC><<<p->ctas, kBinThreads, hsm, st>>>(P, level_out, proj_out)));
         if ((rc = check_launch())) return rc;
     }
-#if !TRIPS_EMIT_SCAN
+#if TRIPS_TILE_SCAN == 0
     {
         StageScope sc(p, 2, st);
         k_tscan<<<1, 1024, hsm, st>>>(P);
@@ -373,20 +383,20 @@ int trips_splat_forward(trips_plan* p, void* ws, float* pyramid, uint32_t flags,
     {
         StageScope sc(p, 3, st);
         const int save = (flags & TRIPS_FWD_SAVE_FOR_BACKWARD) ? 1 : 0;
-        const size_t rsm = (size_t)raster_dyn_smem();
         static bool rattr_dev[kMaxDevices][3][9] = {};
         const int mode = p->coarse ? kRasterOwn : (p->t_min > 0.f ? kRasterTmin : kRasterPlain);
+        const size_t rsm = (size_t)raster_dyn_smem();
         const int dev = current_device();
         std::lock_guard<std::mutex> lk(g_dev_mu);
         bool (&rattr)[3][9] = rattr_dev[dev];
         if (!rattr[mode][p->FC / 4]) {
             const int a = (int)cudaFuncAttributeMaxDynamicSharedMemorySize;
             if (mode == kRasterOwn) {
-                TRIPS_FC_SWITCH(p->FC, (cudaFuncSetAttribute(k_raster<kFC, kRasterOwn>, (cudaFuncAttribute)a, (int)rsm)));
+                TRIPS_FC_SWITCH(p->FC, (cudaFuncSetAttribute(k_raster<kFC, kRasterOwn>, (cudaFuncAttribute)a, raster_dyn_smem())));
             } else if (mode == kRasterTmin) {
-                TRIPS_FC_SWITCH(p->FC, (cudaFuncSetAttribute(k_raster<kFC, kRasterTmin>, (cudaFuncAttribute)a, (int)rsm)));
+                TRIPS_FC_SWITCH(p->FC, (cudaFuncSetAttribute(k_raster<kFC, kRasterTmin>, (cudaFuncAttribute)a, raster_dyn_smem())));
             } else {
-                TRIPS_FC_SWITCH(p->FC, (cudaFuncSetAttribute(k_raster<kFC, kRasterPlain>, (cudaFuncAttribute)a, (int)rsm)));
+                TRIPS_FC_SWITCH(p->FC, (cudaFuncSetAttribute(k_raster<kFC, kRasterPlain>, (cudaFuncAttribute)a, raster_dyn_smem())));
             }
             rattr[mode][p->FC / 4] = true;
         }
@@ -541,9 +551,10 @@ int64_t trips_launch_count(void) { return (int64_t)g_launches.load(); }
 size_t trips_knn_workspace_bytes(int64_t n)
 {
     if (n < 0) return 0;
-    const size_t N = (size_t)(n > 0 ? n : 1), cap = N + 1;
-    return align256(6 * 4) + align256(sizeof(KnnGrid)) + align256(N * 4) + align256((cap + 1) * 4) +
-           align256(cap * 4) + align256(((cap + 1023) / 1024 + 1) * 4) + align256(N * 16);
+    const size_t N = (size_t)(n > 0 ? n : 1);
+    const size_t nblk = (N + kSortBlock - 1) / kSortBlock;
+    return 2 * align256(N * 8) + 2 * align256(N * 4) + align256(256 * nblk * 4) + align256(6 * 4) + align256(4) +
+           align256(N * 16);
 }
 
 int trips_knn_sizes(void* ws, int64_t n, const float* pos, float* size_out, int32_t* nbr_out, void* stream)
@@ -553,42 +564,207 @@ int trips_knn_sizes(void* ws, int64_t n, const float* pos, float* size_out, int3
     if (!aligned(ws, 256) || !aligned(pos, 4) || !aligned(size_out, 4) || !aligned(nbr_out, 4)) return TRIPS_ERR_ALIGN;
     if (n == 0) return TRIPS_OK;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const size_t N = (size_t)n, cap = N + 1;
+    const size_t N = (size_t)n;
     KnnWs W;
     W.n = (int)n;
-    W.cap = (int)cap;
+    W.nblk = (int)((N + kSortBlock - 1) / kSortBlock);
+    W.last_pass = kKnnPasses - 1;
     char* b = static_cast<char*>(ws);
     size_t o = 0;
+    W.keys[0] = reinterpret_cast<uint64_t*>(b + o); o += align256(N * 8);
+    W.keys[1] = reinterpret_cast<uint64_t*>(b + o); o += align256(N * 8);
+    W.vals[0] = reinterpret_cast<uint32_t*>(b + o); o += align256(N * 4);
+    W.vals[1] = reinterpret_cast<uint32_t*>(b + o); o += align256(N * 4);
+    W.hist = reinterpret_cast<uint32_t*>(b + o);    o += align256(256 * (size_t)W.nblk * 4);
     W.bbox = reinterpret_cast<uint32_t*>(b + o);    o += align256(6 * 4);
-    W.grid = reinterpret_cast<KnnGrid*>(b + o);     o += align256(sizeof(KnnGrid));
-    W.cell_of = reinterpret_cast<uint32_t*>(b + o); o += align256(N * 4);
-    W.cnt = reinterpret_cast<uint32_t*>(b + o);     o += align256((cap + 1) * 4);
-    W.cur = reinterpret_cast<uint32_t*>(b + o);     o += align256(cap * 4);
-    W.bsum = reinterpret_cast<uint32_t*>(b + o);    o += align256(((cap + 1023) / 1024 + 1) * 4);
+    W.nfin = reinterpret_cast<uint32_t*>(b + o);    o += align256(4);
     W.pts = reinterpret_cast<float4*>(b + o);
     int rc = cuda_status(cudaMemsetAsync(W.bbox, 0xff, 3 * 4, st));
     if (rc) return rc;
     if ((rc = cuda_status(cudaMemsetAsync(W.bbox + 3, 0, 3 * 4, st)))) return rc;
-    if ((rc = cuda_status(cudaMemsetAsync(W.cnt, 0, (cap + 1) * 4, st)))) return rc;
+    if ((rc = cuda_status(cudaMemsetAsync(W.nfin, 0, 4, st)))) return rc;
     const int pb = (W.n + 255) / 256;
-    k_knn_bbox<<<std::min(pb, 148 * 8), 256, 0, st>>>(W, pos);
+    k_bbox<<<std::min(pb, 148 * 8), 256, 0, st>>>(W, pos);
     if ((rc = check_launch())) return rc;
-    k_knn_setup<<<1, 1, 0, st>>>(W);
+    k_knn_codes<<<pb, 256, 0, st>>>(W, pos);
     if ((rc = check_launch())) return rc;
-    k_knn_count<<<pb, 256, 0, st>>>(W, pos);
+    for (int pass = 0; pass < kKnnPasses; ++pass) {       // even count: sorted codes/indices in [0]
+        k_sort_hist<<<W.nblk, 256, 0, st>>>(W, pass);
+        if ((rc = check_launch())) return rc;
+        k_sort_scan<<<1, 1024, 0, st>>>(W);
+        if ((rc = check_launch())) return rc;
+        k_sort_scatter<<<W.nblk, 256, 0, st>>>(W, pass, nullptr);
+        if ((rc = check_launch())) return rc;
+    }
+    k_knn_gather<<<pb, 256, 0, st>>>(W, pos);
     if ((rc = check_launch())) return rc;
-    const int sb = (int)((cap + 1023) / 1024);       // upper bound of the scan blocks
-    k_knn_scan_a<<<sb, 1024, 0, st>>>(W);
-    if ((rc = check_launch())) return rc;
-    k_knn_scan_b<<<1, 1024, 0, st>>>(W);
-    if ((rc = check_launch())) return rc;
-    k_knn_scan_c<<<sb, 1024, 0, st>>>(W);
-    if ((rc = check_launch())) return rc;
-    k_knn_fill<<<pb, 256, 0, st>>>(W, pos);
-    if ((rc = check_launch())) return rc;
-    k_knn_query<<<pb, 256, 0, st>>>(W, pos, size_out, nbr_out);
+    k_knn_query<<<pb, 256, 0, st>>>(W, size_out, nbr_out);
     return check_launch();
 }
+
+// ----------------------------------------------------------------------------- decoder
+
+namespace {
+
+constexpr int kDecHiddenH = 32;
+
+int64_t dec_layer_params(int C) { return 2 * ((int64_t)kDecHiddenH * C * 9 + kDecHiddenH) + (int64_t)kDecHiddenH * C; }
+int dec_in_channels(const trips_plan* p, int l) { return l == p->n_layers - 1 ? p->F + 1 : kDecHiddenH + p->F + 1; }
+
+struct DecWsLayout {
+    size_t wpack, X, Y0, Y1, bytes;
+};
+
+DecWsLayout dec_ws_layout(const trips_plan* p)
+{
+    DecWsLayout o;
+    size_t b = 0;
+    o.wpack = b; b = align256(b + (size_t)p->n_layers * kDecTaps * kDecN * kDecXC * 2);
+    o.X = b;     b = align256(b + (size_t)p->L[0].H * p->L[0].W * kDecXC * 2);
+    const size_t ysz = p->n_layers > 1 ? (size_t)p->L[1].H * p->L[1].W * kDecHidden * 4 : 256;
+    o.Y0 = b;    b = align256(b + ysz);
+    o.Y1 = b;    b = align256(b + ysz);
+    o.bytes = b;
+    return o;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 dec_encoder()
+{
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+        cudaGetLastError();
+    });
+    return fn;
+}
+
+}  // namespace
+
+int64_t trips_decoder_param_count(const trips_plan* p, int32_t out_channels)
+{
+    if (!p || out_channels < 1 || out_channels > kDecMaxOut) return -1;
+    int64_t n = 0;
+    for (int l = 0; l < p->n_layers; ++l) n += dec_layer_params(dec_in_channels(p, l));
+    return n + (int64_t)out_channels * kDecHiddenH + out_channels;
+}
+
+size_t trips_decoder_workspace_bytes(const trips_plan* p)
+{
+    return p ? dec_ws_layout(p).bytes : 0;
+}
+
+int trips_decode(const trips_plan* p, void* dws, const float* params, int32_t out_channels, const float* pyramid,
+                 float* out, void* stream)
+{
+    if (!p || !dws || !params || !pyramid || !out || out_channels < 1 || out_channels > kDecMaxOut) return TRIPS_ERR_ARG;
+    if (p->F + 1 > kDecXC - kDecHidden) return TRIPS_ERR_ARG;            // pyramid channels must fit X
+    if ((int64_t)p->L[0].H * p->L[0].W * (kDecXC / 8) >= (int64_t(1) << 31)) return TRIPS_ERR_ARG;
+    if (!aligned(dws, 256) || !aligned(params, 4) || !aligned(pyramid, 4) || !aligned(out, 4)) return TRIPS_ERR_ALIGN;
+    PFN_cuTensorMapEncodeTiled_v12000 encode = dec_encoder();
+    if (!encode) {
+        snprintf(g_msg, sizeof(g_msg), "TRIPS_ERR_CUDA: cuTensorMapEncodeTiled unavailable");
+        return TRIPS_ERR_CUDA;
+    }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const DecWsLayout wl = dec_ws_layout(p);
+    char* b = static_cast<char*>(dws);
+    DecParams D;
+    memset(&D, 0, sizeof(D));
+    D.n_layers = p->n_layers;
+    D.F = p->F;
+    D.out_ch = out_channels;
+    int64_t o = 0;
+    for (int l = 0; l < p->n_layers; ++l) {
+        DecLayer& L = D.L[l];
+        L.H = p->L[l].H;
+        L.W = p->L[l].W;
+        L.Hc = l + 1 < p->n_layers ? p->L[l + 1].H : 0;
+        L.Wc = l + 1 < p->n_layers ? p->L[l + 1].W : 0;
+        L.pyr_off = p->L[l].float_off;
+        L.prm_off = o;
+        L.C = dec_in_channels(p, l);
+        L.coarsest = l == p->n_layers - 1;
+        o += dec_layer_params(L.C);
+    }
+    D.prm_out = o;
+    D.prm = params;
+    D.pyramid = pyramid;
+    D.wpack = reinterpret_cast<__half*>(b + wl.wpack);
+    D.X = reinterpret_cast<__half*>(b + wl.X);
+    D.Y[0] = reinterpret_cast<float*>(b + wl.Y0);
+    D.Y[1] = reinterpret_cast<float*>(b + wl.Y1);
+    D.out = out;
+
+    CUtensorMap tmB;
+    {
+        const cuuint64_t dims[2] = {(cuuint64_t)kDecXC, (cuuint64_t)p->n_layers * kDecTaps * kDecN};
+        const cuuint64_t strides[1] = {(cuuint64_t)kDecXC * 2};
+        const cuuint32_t box[2] = {(cuuint32_t)kDecXC, (cuuint32_t)kDecN};
+        const cuuint32_t estr[2] = {1, 1};
+        if (encode(&tmB, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, D.wpack, dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+            snprintf(g_msg, sizeof(g_msg), "TRIPS_ERR_CUDA: weight tensor map");
+            return TRIPS_ERR_CUDA;
+        }
+    }
+    static bool attr_dev[kMaxDevices] = {};
+    {
+        const int dev = current_device();
+        std::lock_guard<std::mutex> lk(g_dev_mu);
+        if (!attr_dev[dev]) {
+            int rc = cuda_status(cudaFuncSetAttribute(k_dec_conv, cudaFuncAttributeMaxDynamicSharedMemorySize, kDecSmem));
+            if (rc) return rc;
+            attr_dev[dev] = true;
+        }
+    }
+    int rc;
+    {
+        const int64_t tot = (int64_t)p->n_layers * kDecTaps * kDecN * kDecXC;
+        k_dec_pack<<<(int)std::min<int64_t>((tot + 255) / 256, 148 * 16), 256, 0, st>>>(D);
+        if ((rc = check_launch())) return rc;
+    }
+    const int sms = num_sms();
+    for (int l = p->n_layers - 1; l >= 0; --l) {
+        const DecLayer& L = D.L[l];
+        const int64_t work = (int64_t)L.H * L.W * (kDecXC / 8);
+        k_dec_prep<<<(int)((work + 255) / 256), 256, 0, st>>>(D, l);
+        if ((rc = check_launch())) return rc;
+        CUtensorMap tmX;
+        const cuuint64_t dims[3] = {(cuuint64_t)kDecXC, (cuuint64_t)L.W, (cuuint64_t)L.H};
+        const cuuint64_t strides[2] = {(cuuint64_t)kDecXC * 2, (cuuint64_t)L.W * kDecXC * 2};
+        const cuuint32_t box[3] = {(cuuint32_t)kDecXC, (cuuint32_t)kDecM, 1};
+        const cuuint32_t estr[3] = {1, 1, 1};
+        if (encode(&tmX, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, D.X, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+            snprintf(g_msg, sizeof(g_msg), "TRIPS_ERR_CUDA: activation tensor map");
+            return TRIPS_ERR_CUDA;
+        }
+        const int ntiles = L.H * ((L.W + kDecM - 1) / kDecM);
+        k_dec_conv<<<std::min(ntiles, sms), kDecThreads, kDecSmem, st>>>(tmX, tmB, D, l);
+        if ((rc = check_launch())) return rc;
+    }
+    return TRIPS_OK;
+}
+
+#ifdef TRIPS_KNN_STATS
+// experiment builds only: kNN query counters (see knn.cuh)
+int trips_debug_knn_stats(unsigned long long* host4, int reset)
+{
+    if (cudaMemcpyFromSymbol(host4, g_knn_stats, 4 * sizeof(unsigned long long)) != cudaSuccess) return TRIPS_ERR_CUDA;
+    if (reset) {
+        unsigned long long z[4] = {0, 0, 0, 0};
+        cudaMemcpyToSymbol(g_knn_stats, z, sizeof(z));
+    }
+    return TRIPS_OK;
+}
+#endif
 
 #ifdef TRIPS_PHASE_CLOCK
 // experiment builds only: k_raster per-phase clocks (see kernels.cuh)
@@ -622,6 +798,7 @@ int trips_morton_order(void* ws, int64_t n, const float* pos, int32_t* perm_out,
     MortonWs W;
     W.n = (int)n;
     W.nblk = (int)((N + kSortBlock - 1) / kSortBlock);
+    W.last_pass = 3;
     char* b = static_cast<char*>(ws);
     size_t o = 0;
     W.keys[0] = reinterpret_cast<uint32_t*>(b + o); o += align256(N * 4);

@@ -59,3 +59,34 @@ def test_surface_cloud_sampled(dev):
     assert np.array_equal(nb[q], nbo)
     assert np.array_equal(s[q].view(np.uint32), so.view(np.uint32))
     assert s.min() >= 0 and np.isfinite(s).all()
+
+
+def test_clusters_duplicates_and_wide_extent(dev):
+    """Morton-window edge cases: dense clusters far apart (octree boundaries between a point and
+    its neighbours), 3000 copies of one point (ties broken by index), a huge-extent outlier pair,
+    and tiny clouds where the window covers everything."""
+    rng = np.random.default_rng(5)
+    cl = [rng.normal(size=(800, 3)) * 1e-3 + rng.uniform(-10, 10, 3) for _ in range(6)]
+    dup = np.repeat(np.array([[0.25, -0.5, 3.0]]), 3000, 0)
+    wide = np.array([[1e30, 0, 0], [-1e30, 5, 5], [1e30, 1, 0]])
+    p = np.concatenate(cl + [dup, wide]).astype(np.float32)
+    p = p[rng.permutation(len(p))]
+    s, nb = run(p, dev)
+    so, nbo = oracle.knn4(p)
+    assert np.array_equal(nb, nbo) and np.array_equal(s.view(np.uint32), so.view(np.uint32))
+    for n in (2, 3, 5, 9, 17, 18, 40):
+        q = rng.normal(size=(n, 3)).astype(np.float32)
+        s, nb = run(q, dev)
+        so, nbo = oracle.knn4(q)
+        assert np.array_equal(nb, nbo) and np.array_equal(s.view(np.uint32), so.view(np.uint32))
+
+
+def test_c4_cloud_full_size_sampled(dev):
+    """The bench's kNN workload: the 8M-point C4 cloud, sampled queries against the brute force."""
+    sc = scenes.make_config("C4", n_views=1)
+    s, nb = run(sc.pos, dev)
+    q = np.random.default_rng(2).choice(sc.n, 200, replace=False)
+    so, nbo = oracle.knn4(sc.pos, queries=q)
+    assert np.array_equal(nb[q], nbo)
+    assert np.array_equal(s[q].view(np.uint32), so.view(np.uint32))
+    assert s.min() >= 0 and np.isfinite(s).all()

@@ -13,6 +13,13 @@ for a in "$@"; do
         --log-file gpurun_out/knn_launches.csv python tools/knn_time.py > /dev/null 2>&1; echo "knnncu rc=$?" ;;
     knnst) TRIPS_LIB=build/var/knnst.so python tools/knn_stats.py ;;
     dectest:*) v=${a#dectest:}; TRIPS_LIB=build/var/$v.so timeout 900 python -m pytest tests/test_gpu_decoder.py -q -x 2>&1 | tail -15 ;;
+    knntime:*) v=${a#knntime:}; TRIPS_LIB=build/var/$v.so python tools/knn_time.py ;;
+    dectime:*) v=${a#dectime:}; TRIPS_LIB=build/var/$v.so python tools/dec_time.py; TRIPS_LIB=build/var/$v.so python tools/dec_time.py --W 3840 --H 2160 ;;
+    knntest:*) v=${a#knntest:}; TRIPS_LIB=build/var/$v.so timeout 900 python -m pytest tests/test_gpu_knn.py -q 2>&1 | tail -3 ;;
+    decncu:*) v=${a#decncu:}; TRIPS_LIB=build/var/$v.so ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_dec" -c 12 --csv \
+        --log-file gpurun_out/dec_launches.csv python tools/dec_time.py --iters 1 > /dev/null 2>&1; echo "decncu rc=$?" ;;
+    decfull:*) v=${a#decfull:}; TRIPS_LIB=build/var/$v.so ncu --set full --clock-control none --import-source on -k regex:"k_dec_conv" -s 3 -c 1 \
+        -o gpurun_out/ncu_dec -f python tools/dec_time.py --iters 1 > /dev/null 2>&1; echo "decfull rc=$?" ;;
     knn) timeout 900 python -m pytest tests/test_gpu_knn.py -q 2>&1 | tail -5; python tools/knn_time.py ;;
     ncu:*) v=${a#ncu:}; k=${NCU_K:-k_raster}; TRIPS_LIB=build/var/$v.so ncu --set full --clock-control none --import-source on \
         -k regex:$k -s 1 -c 1 -o gpurun_out/ncu_$v -f python tools/prof_views.py --views 2 --order morton > /dev/null 2>&1; echo "ncu $v rc=$?" ;;
