@@ -162,56 +162,78 @@ __global__ void __launch_bounds__(256) k_dec_pack(DecParams D)
     }
 }
 
-// k_dec_prep: X_l (see the header).  One thread per (pixel, 8-channel group): 16-byte stores.
+// k_dec_prep: X_l (see the header).  One CTA per 32 x 16 output block: the block's source
+// region of y_{l+1} (at most 18 x 10 pixels x 32 channels) is staged in shared memory with
+// coalesced 16-byte loads, so every source value leaves L2 once instead of once per output pixel
+// that interpolates it; then one thread per (pixel, 8-channel group) writes 16 bytes of X_l.
+constexpr int kPrepW = 32, kPrepH = 16;
+constexpr int kPrepSW = kPrepW / 2 + 2, kPrepSH = kPrepH / 2 + 2;
 __global__ void __launch_bounds__(256) k_dec_prep(DecParams D, int l)
 {
+    __shared__ __align__(16) float s_y[kPrepSH * kPrepSW * kDecHidden];
     const DecLayer& L = D.L[l];
     const int npx = L.H * L.W;                       // < 2^31 / 8 (checked on the host)
-    const int e = blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= npx * (kDecXC / 8)) return;
-    const int grp = e & (kDecXC / 8 - 1);
-    const int p = e >> 3;
-    const int y = p / L.W, x = p - y * L.W;
-    float v[8];
-    if (grp < kDecHidden / 8) {
-        if (L.coarsest) {
+    const int x0 = blockIdx.x * kPrepW, y0 = blockIdx.y * kPrepH;
+    // source window: rows sy0 .. sy0 + SH - 1 (clamped into the layer), same for columns
+    const int sx0 = max(0, x0 / 2 - 1), sy0 = max(0, y0 / 2 - 1);
+    if (!L.coarsest) {
+        const float* Yc = D.Y[(l + 1) & 1];
+        for (int e = threadIdx.x; e < kPrepSH * kPrepSW * (kDecHidden / 4); e += blockDim.x) {
+            const int c4 = e & (kDecHidden / 4 - 1);
+            const int px = e >> 3;
+            const int ry = px / kPrepSW, rx = px - ry * kPrepSW;
+            const int sy = min(sy0 + ry, L.Hc - 1), sx = min(sx0 + rx, L.Wc - 1);
+            reinterpret_cast<float4*>(s_y)[e] =
+                __ldg(reinterpret_cast<const float4*>(Yc + ((int64_t)sy * L.Wc + sx) * kDecHidden) + c4);
+        }
+        __syncthreads();
+    }
+    for (int it = threadIdx.x; it < kPrepW * kPrepH * (kDecXC / 8); it += blockDim.x) {
+        const int grp = it & (kDecXC / 8 - 1);
+        const int q = it >> 3;
+        const int y = y0 + q / kPrepW, x = x0 + (q & (kPrepW - 1));
+        if (y >= L.H || x >= L.W) continue;
+        const int p = y * L.W + x;
+        float v[8];
+        if (grp < kDecHidden / 8) {
+            if (L.coarsest) {
 #pragma unroll
-            for (int j = 0; j < 8; ++j) v[j] = 0.f;
-        } else {
-            // bilinear 2x, half-pixel centres: output i samples (i + 0.5) / 2 - 0.5 >= 0 (clamped)
-            const float* Yc = D.Y[(l + 1) & 1];
-            const float sy = fmaxf((y + 0.5f) * 0.5f - 0.5f, 0.f), sx = fmaxf((x + 0.5f) * 0.5f - 0.5f, 0.f);
-            const int y0 = min((int)sy, L.Hc - 1), x0 = min((int)sx, L.Wc - 1);
-            const int y1 = min(y0 + 1, L.Hc - 1), x1 = min(x0 + 1, L.Wc - 1);
-            const float ly = sy - (float)y0, lx = sx - (float)x0;
-            const float4* a = reinterpret_cast<const float4*>(Yc + ((int64_t)y0 * L.Wc + x0) * kDecHidden + grp * 8);
-            const float4* b = reinterpret_cast<const float4*>(Yc + ((int64_t)y0 * L.Wc + x1) * kDecHidden + grp * 8);
-            const float4* c = reinterpret_cast<const float4*>(Yc + ((int64_t)y1 * L.Wc + x0) * kDecHidden + grp * 8);
-            const float4* d = reinterpret_cast<const float4*>(Yc + ((int64_t)y1 * L.Wc + x1) * kDecHidden + grp * 8);
+                for (int j = 0; j < 8; ++j) v[j] = 0.f;
+            } else {
+                // bilinear 2x, half-pixel centres: output i samples (i + 0.5) / 2 - 0.5 >= 0 (clamped)
+                const float sy = fmaxf((y + 0.5f) * 0.5f - 0.5f, 0.f), sx = fmaxf((x + 0.5f) * 0.5f - 0.5f, 0.f);
+                const int iy0 = min((int)sy, L.Hc - 1), ix0 = min((int)sx, L.Wc - 1);
+                const int iy1 = min(iy0 + 1, L.Hc - 1), ix1 = min(ix0 + 1, L.Wc - 1);
+                const float ly = sy - (float)iy0, lx = sx - (float)ix0;
+                const float4* a = reinterpret_cast<const float4*>(s_y + ((iy0 - sy0) * kPrepSW + (ix0 - sx0)) * kDecHidden + grp * 8);
+                const float4* b = reinterpret_cast<const float4*>(s_y + ((iy0 - sy0) * kPrepSW + (ix1 - sx0)) * kDecHidden + grp * 8);
+                const float4* c = reinterpret_cast<const float4*>(s_y + ((iy1 - sy0) * kPrepSW + (ix0 - sx0)) * kDecHidden + grp * 8);
+                const float4* d = reinterpret_cast<const float4*>(s_y + ((iy1 - sy0) * kPrepSW + (ix1 - sx0)) * kDecHidden + grp * 8);
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const float4 A = a[h], B = b[h], C = c[h], Dd = d[h];
-                const float r0[4] = {A.x, A.y, A.z, A.w}, r1[4] = {B.x, B.y, B.z, B.w};
-                const float r2[4] = {C.x, C.y, C.z, C.w}, r3[4] = {Dd.x, Dd.y, Dd.z, Dd.w};
+                for (int h = 0; h < 2; ++h) {
+                    const float4 A = a[h], B = b[h], C = c[h], Dd = d[h];
+                    const float r0[4] = {A.x, A.y, A.z, A.w}, r1[4] = {B.x, B.y, B.z, B.w};
+                    const float r2[4] = {C.x, C.y, C.z, C.w}, r3[4] = {Dd.x, Dd.y, Dd.z, Dd.w};
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const float top = r0[j] * (1.f - lx) + r1[j] * lx;
-                    const float bot = r2[j] * (1.f - lx) + r3[j] * lx;
-                    v[4 * h + j] = top * (1.f - ly) + bot * ly;
+                    for (int j = 0; j < 4; ++j) {
+                        const float top = r0[j] * (1.f - lx) + r1[j] * lx;
+                        const float bot = r2[j] * (1.f - lx) + r3[j] * lx;
+                        v[4 * h + j] = top * (1.f - ly) + bot * ly;
+                    }
                 }
             }
-        }
-    } else {
+        } else {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const int ch = (grp * 8 + j) - kDecHidden;
-            v[j] = ch <= D.F ? __ldg(D.pyramid + L.pyr_off + (int64_t)ch * npx + p) : 0.f;
+            for (int j = 0; j < 8; ++j) {
+                const int ch = (grp * 8 + j) - kDecHidden;
+                v[j] = ch <= D.F ? __ldg(D.pyramid + L.pyr_off + (int64_t)ch * npx + p) : 0.f;
+            }
         }
+        __half2 h2[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) h2[j] = __floats2half2_rn(v[2 * j], v[2 * j + 1]);
+        *reinterpret_cast<uint4*>(D.X + (int64_t)p * kDecXC + grp * 8) = *reinterpret_cast<uint4*>(h2);
     }
-    __half2 h2[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) h2[j] = __floats2half2_rn(v[2 * j], v[2 * j + 1]);
-    *reinterpret_cast<uint4*>(D.X + (int64_t)p * kDecXC + grp * 8) = *reinterpret_cast<uint4*>(h2);
 }
 
 // fast-math activations (ex2.approx based): |error| ~ 1e-7 absolute, far inside the fp16-operand

@@ -212,49 +212,99 @@ __device__ __forceinline__ uint64_t knn_bigmin(uint64_t c, uint64_t zmin, uint64
 
 __global__ void __launch_bounds__(256) k_knn_query(KnnWs W, float* __restrict__ size_out, int32_t* __restrict__ nbr_out)
 {
+    constexpr unsigned kAll = 0xffffffffu;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= W.n) return;
+    const int lane = threadIdx.x & 31;
+    const bool live = k < W.n;                       // no early return: the warp cooperates below
     const int nf = (int)*W.nfin;
     const uint64_t* __restrict__ codes = W.keys[0];
     const float4* __restrict__ pts = W.pts;
-    const float4 p = pts[k];
+    const float4 p = live ? pts[k] : make_float4(0.f, 0.f, 0.f, 0.f);
     const uint32_t i = __float_as_uint(p.w);
     float bd[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
     uint32_t bj[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};
     int nb = 0;
-    auto cand = [&](int j) {
-        const float4 q = pts[j];
-        const float ddx = __fsub_rn(q.x, p.x), ddy = __fsub_rn(q.y, p.y), ddz = __fsub_rn(q.z, p.z);
+    auto cand_pt = [&](float qx, float qy, float qz, uint32_t jj) {
+        const float ddx = __fsub_rn(qx, p.x), ddy = __fsub_rn(qy, p.y), ddz = __fsub_rn(qz, p.z);
         float d2 = __fadd_rn(__fmul_rn(ddx, ddx), __fmul_rn(ddy, ddy));
         d2 = __fadd_rn(d2, __fmul_rn(ddz, ddz));
-        const uint32_t jj = __float_as_uint(q.w);
         ++nb;
         TRIPS_KNN_COUNT(0, 1);
         if (d2 < bd[3] || (d2 == bd[3] && jj < bj[3])) knn_insert(bd, bj, d2, jj);
     };
-    if (k < nf) {
-        const int w0 = max(0, k - kKnnWin), w1 = min(nf - 1, k + kKnnWin);
+    auto cand = [&](int j) {
+        const float4 q = pts[j];
+        cand_pt(q.x, q.y, q.z, __float_as_uint(q.w));
+    };
+    const bool fin = live && k < nf;
+    const int w0 = max(0, k - kKnnWin), w1 = min(nf - 1, k + kKnnWin);
+    if (fin)
         for (int j = w0; j <= w1; ++j)
             if (j != k) cand(j);
-        if (w0 > 0 || w1 < nf - 1) {
-            // the window holds >= kKnnWin >= 4 others, so bd[3] is finite: every point with a
-            // smaller (d^2, j) key lies within r of p (fp32 rounding of d^2 covered by the factor),
-            // hence inside the quantised box [qlo, qhi] (+-1 step for the quantisation rounding).
-            // Its points are the sorted positions whose code lies in [code(qlo), code(qhi)] AND
-            // whose per-axis bits lie in the box: scan that code range, jumping over the stretches
-            // of the curve outside the box with BIGMIN (the next code >= c inside the box).
-            const KnnQuant Q = knn_quant(W.bbox);
-            const double r = sqrt((double)bd[3]) * (1.0 + 1e-5);
-            const double pp[3] = {p.x, p.y, p.z};
-            int qlo[3], qhi[3];
+    // the window holds >= kKnnWin >= 4 others unless it covers every finite point, so bd[3] is
+    // finite: every point with a smaller (d^2, j) key lies within r of p (fp32 rounding of d^2
+    // covered by the factor), hence inside the quantised box [qlo, qhi] (+-1 step for the
+    // quantisation rounding)
+    const bool need = fin && (w0 > 0 || w1 < nf - 1);
+    int qlo[3] = {0, 0, 0}, qhi[3] = {-1, -1, -1};
+    if (need) {
+        const KnnQuant Q = knn_quant(W.bbox);
+        const double r = sqrt((double)bd[3]) * (1.0 + 1e-5);
+        const double pp[3] = {p.x, p.y, p.z};
 #pragma unroll
-            for (int a = 0; a < 3; ++a) {
-                qlo[a] = max(0, knn_q(pp[a] - r, Q.lo[a], Q.scale) - 1);
-                qhi[a] = min((1 << kKnnBits) - 1, knn_q(pp[a] + r, Q.lo[a], Q.scale) + 1);
+        for (int a = 0; a < 3; ++a) {
+            qlo[a] = max(0, knn_q(pp[a] - r, Q.lo[a], Q.scale) - 1);
+            qhi[a] = min((1 << kKnnBits) - 1, knn_q(pp[a] + r, Q.lo[a], Q.scale) + 1);
+        }
+        TRIPS_KNN_COUNT(3, 1);
+        TRIPS_KNN_COUNT(1, (uint64_t)(qhi[0] - qlo[0] + 1) * (uint64_t)(qhi[1] - qlo[1] + 1));
+    }
+    // Warp mode: the 32 queries of a warp are neighbours on the curve, so their boxes overlap.
+    // When the union box is compact the warp scans it once, cooperatively: 32 consecutive sorted
+    // positions per step (coalesced), each in-box point broadcast to every lane, BIGMIN jumps
+    // shared by the warp.  Otherwise (the warp straddles a far jump of the curve) each lane scans
+    // its own box.  Either way every point of a lane's box is evaluated exactly once (window
+    // positions skipped), so the top-4 is exact.
+    const unsigned act = __ballot_sync(kAll, need);
+    if (act) {
+        int ulo[3], uhi[3], lext = 0, uext = 0;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            ulo[a] = __reduce_min_sync(kAll, need ? qlo[a] : (1 << kKnnBits));
+            uhi[a] = __reduce_max_sync(kAll, need ? qhi[a] : -1);
+            lext = max(lext, qhi[a] - qlo[a]);
+            uext = max(uext, uhi[a] - ulo[a]);
+        }
+        lext = __reduce_max_sync(kAll, need ? lext : 0);
+        if (uext <= 3 * lext + 64) {
+            const uint64_t zmin = knn_code(ulo[0], ulo[1], ulo[2]), zmax = knn_code(uhi[0], uhi[1], uhi[2]);
+            const int k0 = __shfl_sync(kAll, k, __ffs(act) - 1);
+            int j = knn_lower_bound(codes, nf, zmin, k0);          // warp-uniform
+            while (j < nf) {
+                const int pos = j + lane;
+                const uint64_t c = pos < nf ? codes[pos] : ~0ull;
+                const bool inb = c <= zmax && knn_in_box(c, zmin, zmax);
+                const float4 q = inb ? pts[pos] : make_float4(0.f, 0.f, 0.f, 0.f);
+                unsigned m = __ballot_sync(kAll, inb);
+                while (m) {
+                    const int b = __ffs(m) - 1;
+                    m &= m - 1;
+                    const float qx = __shfl_sync(kAll, q.x, b), qy = __shfl_sync(kAll, q.y, b);
+                    const float qz = __shfl_sync(kAll, q.z, b), qw = __shfl_sync(kAll, q.w, b);
+                    const int pb = j + b;
+                    if (need && pb != k && (pb < w0 || pb > w1)) cand_pt(qx, qy, qz, __float_as_uint(qw));
+                }
+                if (__any_sync(kAll, c > zmax)) break;              // the code range ends in this step
+                if (__shfl_sync(kAll, inb ? 1 : 0, 31)) { j += 32; continue; }
+                const uint64_t bm = knn_bigmin(__shfl_sync(kAll, c, 31), zmin, zmax);
+                TRIPS_KNN_COUNT(2, 1);
+                if (bm == ~0ull) break;
+                j = knn_lower_bound(codes, nf, bm, j + 31);
             }
+        } else if (need) {
+            // this lane's own box: scan [code(qlo), code(qhi)], jumping over the stretches of the
+            // curve outside the box with BIGMIN (the next code >= c inside the box)
             const uint64_t zmin = knn_code(qlo[0], qlo[1], qlo[2]), zmax = knn_code(qhi[0], qhi[1], qhi[2]);
-            TRIPS_KNN_COUNT(3, 1);
-            TRIPS_KNN_COUNT(1, (uint64_t)(qhi[0] - qlo[0] + 1) * (uint64_t)(qhi[1] - qlo[1] + 1));
             int j = knn_lower_bound(codes, nf, zmin, k);
             while (j < nf) {
                 const uint64_t c = codes[j];
@@ -271,6 +321,7 @@ __global__ void __launch_bounds__(256) k_knn_query(KnnWs W, float* __restrict__ 
             }
         }
     }
+    if (!live) return;
     const int K = nb < 4 ? nb : 4;
     float sz = 0.f;
 #pragma unroll

@@ -732,8 +732,7 @@ int trips_decode(const trips_plan* p, void* dws, const float* params, int32_t ou
     const int sms = num_sms();
     for (int l = p->n_layers - 1; l >= 0; --l) {
         const DecLayer& L = D.L[l];
-        const int64_t work = (int64_t)L.H * L.W * (kDecXC / 8);
-        k_dec_prep<<<(int)((work + 255) / 256), 256, 0, st>>>(D, l);
+        k_dec_prep<<<dim3((L.W + kPrepW - 1) / kPrepW, (L.H + kPrepH - 1) / kPrepH), 256, 0, st>>>(D, l);
         if ((rc = check_launch())) return rc;
         CUtensorMap tmX;
         const cuuint64_t dims[3] = {(cuuint64_t)kDecXC, (cuuint64_t)L.W, (cuuint64_t)L.H};
