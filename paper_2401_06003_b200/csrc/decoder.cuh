@@ -36,14 +36,16 @@ constexpr int kDecXC = 64;                 // X channels: 32 upsampled + F + 1 p
 constexpr int kDecN = 96;                  // GEMM N: f (32) | g (32) | bypass (32)
 constexpr int kDecM = 128;                 // pixels per tile (one UMMA M)
 constexpr int kDecTaps = 9;
-constexpr int kDecStages = 4;
+#ifndef TRIPS_DEC_STAGES
+#define TRIPS_DEC_STAGES 6
+#endif
+constexpr int kDecStages = TRIPS_DEC_STAGES;    // A-tap ring depth (smem: 108 KB B + 16 KB per stage)
 constexpr int kDecABytes = kDecM * kDecXC * 2;          // 16 KB per tap
 constexpr int kDecBBytes = kDecN * kDecXC * 2;          // 12 KB per tap
 constexpr int kDecEpiWarps = 8;                         // 2 per TMEM lane quarter (16 channels each)
 constexpr int kDecThreads = 64 + 32 * kDecEpiWarps;     // TMA warp, MMA warp, epilogue warps
 constexpr int kDecMaxOut = 32;
-constexpr int kDecProjBytes = 4 * 32 * kDecMaxOut * 4;  // final layer: partial projections of the upper halves
-constexpr int kDecSmem = 1024 + kDecTaps * kDecBBytes + kDecStages * kDecABytes + kDecProjBytes + 256;
+constexpr int kDecSmem = 1024 + kDecTaps * kDecBBytes + kDecStages * kDecABytes + 256;
 
 // ----------------------------------------------------------------------------- PTX wrappers
 
@@ -113,7 +115,6 @@ __device__ __forceinline__ void dec_tmem_ld16(uint32_t taddr, uint32_t (&r)[16])
                  : "r"(taddr));
 }
 __device__ __forceinline__ void dec_tmem_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-__device__ __forceinline__ void dec_bar_pair(int id) { asm volatile("bar.sync %0, 64;" :: "r"(id) : "memory"); }
 
 // ----------------------------------------------------------------------------- parameters
 
@@ -250,8 +251,7 @@ __global__ void __launch_bounds__(kDecThreads, 1) k_dec_conv(const __grid_consta
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dec_smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sB = smem;                                           // 9 x 12 KB
     uint8_t* sA = smem + kDecTaps * kDecBBytes;                   // stages x 16 KB
-    float* sProj = reinterpret_cast<float*>(sA + kDecStages * kDecABytes);   // [4][32][out]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sA + kDecStages * kDecABytes + kDecProjBytes);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sA + kDecStages * kDecABytes);
     uint64_t* full = bars;                                        // [stages]
     uint64_t* empty = bars + kDecStages;                          // [stages]
     uint64_t* tfull = bars + 2 * kDecStages;                      // [2]
@@ -333,60 +333,74 @@ __global__ void __launch_bounds__(kDecThreads, 1) k_dec_conv(const __grid_consta
         const float* bg = P + 2 * wsz + kDecHidden + 16 * h;
         const bool last = l == 0;
         float* Yo = D.Y[l & 1];
-        float* proj = sProj + (q * 32 + lane) * kDecMaxOut;
         int it = 0;
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
             const int acc = it & 1;
             const uint32_t aph = (uint32_t)(it >> 1) & 1u;
             dec_mbar_wait(tfull + acc, aph);
             dec_tc_fence_after();
-            const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * kDecN + 16 * h);
-            uint32_t f[16], g[16], b[16];
-            dec_tmem_ld16(ta, f);
-            dec_tmem_ld16(ta + 32, g);
-            dec_tmem_ld16(ta + 64, b);
-            dec_tmem_wait();
-            dec_tc_fence_before();
-            __syncwarp();
-            if (lane == 0) dec_mbar_arrive(tempty + acc);    // TMEM buffer may be refilled
             const int y = tile / xt, x = (tile % xt) * kDecM + 32 * q + lane;
-            float o[16];
-#pragma unroll
-            for (int c = 0; c < 16; ++c)
-                o[c] = dec_elu(__uint_as_float(f[c]) + __ldg(bf + c)) * dec_sigmoid(__uint_as_float(g[c]) + __ldg(bg + c)) +
-                       __uint_as_float(b[c]);
             const int64_t p = (int64_t)y * L.W + x;
+            const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * kDecN);
             if (!last) {
+                // hidden layer: this warp's 16 channels of y_l
+                uint32_t f[16], g[16], b[16];
+                dec_tmem_ld16(ta + 16 * h, f);
+                dec_tmem_ld16(ta + 32 + 16 * h, g);
+                dec_tmem_ld16(ta + 64 + 16 * h, b);
+                dec_tmem_wait();
+                dec_tc_fence_before();
+                __syncwarp();
+                if (lane == 0) dec_mbar_arrive(tempty + acc);    // TMEM buffer may be refilled
+                float o[16];
+#pragma unroll
+                for (int c = 0; c < 16; ++c)
+                    o[c] = dec_elu(__uint_as_float(f[c]) + __ldg(bf + c)) * dec_sigmoid(__uint_as_float(g[c]) + __ldg(bg + c)) +
+                           __uint_as_float(b[c]);
                 if (x < L.W) {
                     float4* dst = reinterpret_cast<float4*>(Yo + p * kDecHidden + 16 * h);
 #pragma unroll
                     for (int c4 = 0; c4 < 4; ++c4) dst[c4] = make_float4(o[4 * c4], o[4 * c4 + 1], o[4 * c4 + 2], o[4 * c4 + 3]);
                 }
             } else {
-                // output projection Wo y + bo: each half projects its 16 channels; the upper half
-                // hands its partial sums to the lower half through shared memory (64-thread barrier
-                // of the warp pair)
-                const float* Wo = D.prm + D.prm_out + 16 * h;
-                const float* bo = D.prm + D.prm_out + (int64_t)D.out_ch * kDecHidden;
-                const int64_t plane = (int64_t)L.H * L.W;
-                if (h == 1) {
-                    for (int oc = 0; oc < D.out_ch; ++oc) {
-                        float sacc = 0.f;
-#pragma unroll
-                        for (int c = 0; c < 16; ++c) sacc = fmaf(__ldg(Wo + oc * kDecHidden + c), o[c], sacc);
-                        proj[oc] = sacc;
-                    }
+                // finest layer: the two warps of a lane quarter take alternate tiles whole (all 32
+                // channels), so the output projection Wo y + bo needs no exchange between them
+                const bool mine = (it & 1) == h;
+                uint32_t f0[16], f1[16], g0[16], g1[16], b0[16], b1[16];
+                if (mine) {
+                    dec_tmem_ld16(ta, f0);
+                    dec_tmem_ld16(ta + 16, f1);
+                    dec_tmem_ld16(ta + 32, g0);
+                    dec_tmem_ld16(ta + 48, g1);
+                    dec_tmem_ld16(ta + 64, b0);
+                    dec_tmem_ld16(ta + 80, b1);
+                    dec_tmem_wait();
                 }
-                dec_bar_pair(1 + q);
-                if (h == 0) {
-                    for (int oc = 0; oc < D.out_ch; ++oc) {
-                        float sacc = __ldg(bo + oc) + proj[oc];
+                dec_tc_fence_before();
+                __syncwarp();
+                if (lane == 0) dec_mbar_arrive(tempty + acc);
+                if (mine) {
+                    const float* bf0 = bf - 16 * h;
+                    const float* bg0 = bg - 16 * h;
+                    float o[32];
 #pragma unroll
-                        for (int c = 0; c < 16; ++c) sacc = fmaf(__ldg(Wo + oc * kDecHidden + c), o[c], sacc);
-                        if (x < L.W) D.out[oc * plane + p] = sacc;
+                    for (int c = 0; c < 16; ++c) {
+                        o[c] = dec_elu(__uint_as_float(f0[c]) + __ldg(bf0 + c)) * dec_sigmoid(__uint_as_float(g0[c]) + __ldg(bg0 + c)) +
+                               __uint_as_float(b0[c]);
+                        o[16 + c] = dec_elu(__uint_as_float(f1[c]) + __ldg(bf0 + 16 + c)) *
+                                        dec_sigmoid(__uint_as_float(g1[c]) + __ldg(bg0 + 16 + c)) + __uint_as_float(b1[c]);
                     }
+                    const float* Wo = D.prm + D.prm_out;
+                    const float* bo = Wo + (int64_t)D.out_ch * kDecHidden;
+                    const int64_t plane = (int64_t)L.H * L.W;
+                    if (x < L.W)
+                        for (int oc = 0; oc < D.out_ch; ++oc) {
+                            float sacc = __ldg(bo + oc);
+#pragma unroll
+                            for (int c = 0; c < 32; ++c) sacc = fmaf(__ldg(Wo + oc * kDecHidden + c), o[c], sacc);
+                            D.out[oc * plane + p] = sacc;
+                        }
                 }
-                dec_bar_pair(1 + q);                         // proj may be rewritten for the next tile
             }
         }
     }

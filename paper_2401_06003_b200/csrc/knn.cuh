@@ -36,6 +36,7 @@ struct KnnWs {
     uint64_t* keys[2];        // [n] codes (sorted into keys[0] after the even number of passes)
     uint32_t* vals[2];        // [n] point index (sorted into vals[0])
     uint32_t* hist;           // [256][nblk]
+    uint32_t* bsum;           // [ceil(256 nblk / 1024)] segment totals of the histogram scan
     uint32_t* bbox;           // [6] orderable float bits (min xyz, max xyz) of the finite points
     uint32_t* nfin;           // [1] finite points (they sort first)
     float4* pts;              // [n] (x, y, z, index bits) in sorted order
@@ -260,10 +261,10 @@ __global__ void __launch_bounds__(256) k_knn_query(KnnWs W, float* __restrict__ 
         TRIPS_KNN_COUNT(1, (uint64_t)(qhi[0] - qlo[0] + 1) * (uint64_t)(qhi[1] - qlo[1] + 1));
     }
     // Warp mode: the 32 queries of a warp are neighbours on the curve, so their boxes overlap.
-    // When the union box is compact the warp scans it once, cooperatively: 32 consecutive sorted
-    // positions per step (coalesced), each in-box point broadcast to every lane, BIGMIN jumps
-    // shared by the warp.  Otherwise (the warp straddles a far jump of the curve) each lane scans
-    // its own box.  Either way every point of a lane's box is evaluated exactly once (window
+    // When the union box is compact the warp scans it once, cooperatively (octree cells located in
+    // parallel, then 32 consecutive sorted positions per step, coalesced, each in-box point
+    // broadcast to every lane).  Otherwise (the warp straddles a far jump of the curve) each lane
+    // scans its own box with BIGMIN jumps.  Either way every point of a lane's box is evaluated exactly once (window
     // positions skipped), so the top-4 is exact.
     const unsigned act = __ballot_sync(kAll, need);
     if (act) {
@@ -277,31 +278,46 @@ __global__ void __launch_bounds__(256) k_knn_query(KnnWs W, float* __restrict__ 
         }
         lext = __reduce_max_sync(kAll, need ? lext : 0);
         if (uext <= 3 * lext + 64) {
+            // the union box is covered by <= 3 x 3 x 3 aligned octree cells of the smallest size that
+            // spans it in 3; each cell is one contiguous code range of the sorted array, located by a
+            // lane of its own (parallel lower_bounds); the warp then sweeps the cells' ranges 32
+            // positions at a time, broadcasting the in-box points
             const uint64_t zmin = knn_code(ulo[0], ulo[1], ulo[2]), zmax = knn_code(uhi[0], uhi[1], uhi[2]);
+            int sh = 0;
+            while (sh < kKnnBits && ((uhi[0] >> sh) - (ulo[0] >> sh) > 2 || (uhi[1] >> sh) - (ulo[1] >> sh) > 2 ||
+                                     (uhi[2] >> sh) - (ulo[2] >> sh) > 2))
+                ++sh;
+            const int nx = (uhi[0] >> sh) - (ulo[0] >> sh) + 1, ny = (uhi[1] >> sh) - (ulo[1] >> sh) + 1;
+            const int ncell = nx * ny * ((uhi[2] >> sh) - (ulo[2] >> sh) + 1);
             const int k0 = __shfl_sync(kAll, k, __ffs(act) - 1);
-            int j = knn_lower_bound(codes, nf, zmin, k0);          // warp-uniform
-            while (j < nf) {
-                const int pos = j + lane;
-                const uint64_t c = pos < nf ? codes[pos] : ~0ull;
-                const bool inb = c <= zmax && knn_in_box(c, zmin, zmax);
-                const float4 q = inb ? pts[pos] : make_float4(0.f, 0.f, 0.f, 0.f);
-                unsigned m = __ballot_sync(kAll, inb);
-                while (m) {
-                    const int b = __ffs(m) - 1;
-                    m &= m - 1;
-                    const float qx = __shfl_sync(kAll, q.x, b), qy = __shfl_sync(kAll, q.y, b);
-                    const float qz = __shfl_sync(kAll, q.z, b), qw = __shfl_sync(kAll, q.w, b);
-                    const int pb = j + b;
-                    if (need && pb != k && (pb < w0 || pb > w1)) cand_pt(qx, qy, qz, __float_as_uint(qw));
-                }
-                if (__any_sync(kAll, c > zmax)) break;              // the code range ends in this step
-                if (__shfl_sync(kAll, inb ? 1 : 0, 31)) { j += 32; continue; }
-                const uint64_t bm = knn_bigmin(__shfl_sync(kAll, c, 31), zmin, zmax);
+            int ca = 0, cb = 0;                                      // this lane's cell: [ca, cb)
+            if (lane < ncell) {
+                const int cx = (ulo[0] >> sh) + lane % nx, cy = (ulo[1] >> sh) + (lane / nx) % ny;
+                const int cz = (ulo[2] >> sh) + lane / (nx * ny);
+                const uint64_t base = knn_code(cx << sh, cy << sh, cz << sh);
+                ca = knn_lower_bound(codes, nf, base, k0);
+                cb = knn_lower_bound(codes, nf, base + (1ull << (3 * sh)), ca < nf ? ca : nf - 1);
                 TRIPS_KNN_COUNT(2, 1);
-                if (bm == ~0ull) break;
-                j = knn_lower_bound(codes, nf, bm, j + 31);
+            }
+            for (int cc = 0; cc < ncell; ++cc) {
+                const int a = __shfl_sync(kAll, ca, cc), b = __shfl_sync(kAll, cb, cc);
+                for (int j = a; j < b; j += 32) {
+                    const int pos = j + lane;
+                    const bool inb = pos < b && knn_in_box(codes[pos], zmin, zmax);
+                    const float4 q = inb ? pts[pos] : make_float4(0.f, 0.f, 0.f, 0.f);
+                    unsigned m = __ballot_sync(kAll, inb);
+                    while (m) {
+                        const int bl = __ffs(m) - 1;
+                        m &= m - 1;
+                        const float qx = __shfl_sync(kAll, q.x, bl), qy = __shfl_sync(kAll, q.y, bl);
+                        const float qz = __shfl_sync(kAll, q.z, bl), qw = __shfl_sync(kAll, q.w, bl);
+                        const int pb = j + bl;
+                        if (need && pb != k && (pb < w0 || pb > w1)) cand_pt(qx, qy, qz, __float_as_uint(qw));
+                    }
+                }
             }
         } else if (need) {
+            TRIPS_KNN_COUNT(3, 1000000);                     // (stats builds: fallback lanes, x 1e6)
             // this lane's own box: scan [code(qlo), code(qhi)], jumping over the stretches of the
             // curve outside the box with BIGMIN (the next code >= c inside the box)
             const uint64_t zmin = knn_code(qlo[0], qlo[1], qlo[2]), zmax = knn_code(qhi[0], qhi[1], qhi[2]);

@@ -23,6 +23,7 @@ struct MortonWs {
     uint32_t* keys[2];
     uint32_t* vals[2];
     uint32_t* hist;          // [256][nblk] digit-major -> exclusive offsets
+    uint32_t* bsum;          // [ceil(256 nblk / 1024)] segment totals of the histogram scan
     uint32_t* bbox;          // [6] orderable float bits: min xyz, max xyz
     int n, nblk;
     int last_pass;           // the scatter of this pass writes the values to final_vals
@@ -116,21 +117,14 @@ __global__ void __launch_bounds__(256) k_sort_hist(WS W, int pass)
     W.hist[(size_t)threadIdx.x * W.nblk + blk] = h[threadIdx.x];
 }
 
-// One CTA: exclusive scan of the digit-major histogram (digit d, block b) in place.  Each thread
-// sums a contiguous run (the run's cache lines stay in L1 between the two passes), one block scan
-// of the 1024 run sums, then each thread rewrites its run as offsets: two passes over the array
-// instead of total / 1024 barrier-separated rounds.
-template <typename WS>
-__global__ void __launch_bounds__(1024) k_sort_scan(WS W)
+// Exclusive scan of the digit-major histogram (digit d, block b) in place, in three launches:
+// k_sort_scan_blocks scans 1024-entry segments and records their totals, k_sort_scan_top scans
+// the totals (one CTA), k_sort_scan_add adds each segment's offset.  (A single CTA walking the
+// ~500k entries at C4 size took ~0.45 ms per pass.)
+__device__ __forceinline__ uint32_t sort_block_excl_scan(uint32_t v, uint32_t* ws, uint32_t* total)
 {
-    __shared__ uint32_t ws[32];
-    const int total = 256 * W.nblk;
-    const int per = (total + blockDim.x - 1) / blockDim.x;
-    const int e0 = min(total, (int)threadIdx.x * per), e1 = min(total, e0 + per);
-    uint32_t sum = 0;
-    for (int e = e0; e < e1; ++e) sum += W.hist[e];
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t x = sum;
+    uint32_t x = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
@@ -148,12 +142,46 @@ __global__ void __launch_bounds__(1024) k_sort_scan(WS W)
         ws[lane] = w;
     }
     __syncthreads();
-    uint32_t run = (warp ? ws[warp - 1] : 0u) + x - sum;
-    for (int e = e0; e < e1; ++e) {
-        const uint32_t v = W.hist[e];
-        W.hist[e] = run;
-        run += v;
+    *total = ws[31];
+    return (warp ? ws[warp - 1] : 0u) + x - v;
+}
+
+template <typename WS>
+__global__ void __launch_bounds__(1024) k_sort_scan_blocks(WS W)
+{
+    __shared__ uint32_t ws[32];
+    const int total = 256 * W.nblk;
+    const int e = blockIdx.x * 1024 + threadIdx.x;
+    const uint32_t v = e < total ? W.hist[e] : 0u;
+    uint32_t tot;
+    const uint32_t ex = sort_block_excl_scan(v, ws, &tot);
+    if (e < total) W.hist[e] = ex;
+    if (threadIdx.x == 0) W.bsum[blockIdx.x] = tot;
+}
+
+template <typename WS>
+__global__ void __launch_bounds__(1024) k_sort_scan_top(WS W)
+{
+    __shared__ uint32_t ws[32];
+    const int nseg = (256 * W.nblk + 1023) / 1024;
+    uint32_t carry = 0;
+    for (int base = 0; base < nseg; base += 1024) {
+        const int e = base + threadIdx.x;
+        const uint32_t v = e < nseg ? W.bsum[e] : 0u;
+        uint32_t tot;
+        const uint32_t ex = sort_block_excl_scan(v, ws, &tot);
+        if (e < nseg) W.bsum[e] = carry + ex;
+        carry += tot;
+        __syncthreads();
     }
+}
+
+template <typename WS>
+__global__ void __launch_bounds__(1024) k_sort_scan_add(WS W)
+{
+    const int total = 256 * W.nblk;
+    const int e = blockIdx.x * 1024 + threadIdx.x;
+    if (e < total) W.hist[e] += W.bsum[blockIdx.x];
 }
 
 // Stable scatter: rounds of 256 consecutive elements; rank = elements of the same digit in

@@ -204,6 +204,19 @@ Params make_params(const trips_plan* p, void* ws)
 
 bool aligned(const void* ptr, size_t a) { return (reinterpret_cast<uintptr_t>(ptr) & (a - 1)) == 0; }
 
+template <typename WS>
+int sort_scan(const WS& W, cudaStream_t st)
+{
+    const int nseg = (256 * W.nblk + 1023) / 1024;
+    int rc;
+    k_sort_scan_blocks<<<nseg, 1024, 0, st>>>(W);
+    if ((rc = check_launch())) return rc;
+    k_sort_scan_top<<<1, 1024, 0, st>>>(W);
+    if ((rc = check_launch())) return rc;
+    k_sort_scan_add<<<nseg, 1024, 0, st>>>(W);
+    return check_launch();
+}
+
 #ifdef TRIPS_FC4_ONLY   // experiment builds (tools/ variants): F <= 4 only, ~6x faster to compile
 #define TRIPS_FC_SWITCH(FC, CALL)                \
     switch (FC) {                                \
@@ -553,8 +566,8 @@ size_t trips_knn_workspace_bytes(int64_t n)
     if (n < 0) return 0;
     const size_t N = (size_t)(n > 0 ? n : 1);
     const size_t nblk = (N + kSortBlock - 1) / kSortBlock;
-    return 2 * align256(N * 8) + 2 * align256(N * 4) + align256(256 * nblk * 4) + align256(6 * 4) + align256(4) +
-           align256(N * 16);
+    return 2 * align256(N * 8) + 2 * align256(N * 4) + align256(256 * nblk * 4) + align256((256 * nblk + 1023) / 1024 * 4) +
+           align256(6 * 4) + align256(4) + align256(N * 16);
 }
 
 int trips_knn_sizes(void* ws, int64_t n, const float* pos, float* size_out, int32_t* nbr_out, void* stream)
@@ -576,6 +589,7 @@ int trips_knn_sizes(void* ws, int64_t n, const float* pos, float* size_out, int3
     W.vals[0] = reinterpret_cast<uint32_t*>(b + o); o += align256(N * 4);
     W.vals[1] = reinterpret_cast<uint32_t*>(b + o); o += align256(N * 4);
     W.hist = reinterpret_cast<uint32_t*>(b + o);    o += align256(256 * (size_t)W.nblk * 4);
+    W.bsum = reinterpret_cast<uint32_t*>(b + o);    o += align256((256 * (size_t)W.nblk + 1023) / 1024 * 4);
     W.bbox = reinterpret_cast<uint32_t*>(b + o);    o += align256(6 * 4);
     W.nfin = reinterpret_cast<uint32_t*>(b + o);    o += align256(4);
     W.pts = reinterpret_cast<float4*>(b + o);
@@ -591,8 +605,7 @@ int trips_knn_sizes(void* ws, int64_t n, const float* pos, float* size_out, int3
     for (int pass = 0; pass < kKnnPasses; ++pass) {       // even count: sorted codes/indices in [0]
         k_sort_hist<<<W.nblk, 256, 0, st>>>(W, pass);
         if ((rc = check_launch())) return rc;
-        k_sort_scan<<<1, 1024, 0, st>>>(W);
-        if ((rc = check_launch())) return rc;
+        if ((rc = sort_scan(W, st))) return rc;
         k_sort_scatter<<<W.nblk, 256, 0, st>>>(W, pass, nullptr);
         if ((rc = check_launch())) return rc;
     }
@@ -783,7 +796,7 @@ size_t trips_morton_workspace_bytes(int64_t n)
     if (n < 0) return 0;
     const size_t N = (size_t)(n > 0 ? n : 1);
     const size_t nblk = (N + kSortBlock - 1) / kSortBlock;
-    return 4 * align256(N * 4) + align256(256 * nblk * 4) + align256(6 * 4);
+    return 4 * align256(N * 4) + align256(256 * nblk * 4) + align256((256 * nblk + 1023) / 1024 * 4) + align256(6 * 4);
 }
 
 int trips_morton_order(void* ws, int64_t n, const float* pos, int32_t* perm_out, void* stream)
@@ -805,6 +818,7 @@ int trips_morton_order(void* ws, int64_t n, const float* pos, int32_t* perm_out,
     W.vals[0] = reinterpret_cast<uint32_t*>(b + o); o += align256(N * 4);
     W.vals[1] = reinterpret_cast<uint32_t*>(b + o); o += align256(N * 4);
     W.hist = reinterpret_cast<uint32_t*>(b + o); o += align256(256 * (size_t)W.nblk * 4);
+    W.bsum = reinterpret_cast<uint32_t*>(b + o); o += align256((256 * (size_t)W.nblk + 1023) / 1024 * 4);
     W.bbox = reinterpret_cast<uint32_t*>(b + o);
     int rc = cuda_status(cudaMemsetAsync(W.bbox, 0xff, 3 * 4, st));
     if (rc) return rc;
@@ -816,8 +830,7 @@ int trips_morton_order(void* ws, int64_t n, const float* pos, int32_t* perm_out,
     for (int pass = 0; pass < 4; ++pass) {
         k_sort_hist<<<W.nblk, 256, 0, st>>>(W, pass);
         if ((rc = check_launch())) return rc;
-        k_sort_scan<<<1, 1024, 0, st>>>(W);
-        if ((rc = check_launch())) return rc;
+        if ((rc = sort_scan(W, st))) return rc;
         k_sort_scatter<<<W.nblk, 256, 0, st>>>(W, pass, reinterpret_cast<uint32_t*>(perm_out));
         if ((rc = check_launch())) return rc;
     }
