@@ -24,6 +24,9 @@ namespace trips {
 #ifndef TRIPS_GROUP8
 #define TRIPS_GROUP8 0
 #endif
+#ifndef TRIPS_PAIR_HASH
+#define TRIPS_PAIR_HASH 0      // measured slower: raster +36 us (blend-loop atomics, 26 KB more smem = less L1)
+#endif
 #ifndef TRIPS_RASTER_CTAS
 #define TRIPS_RASTER_CTAS 3
 #endif
@@ -45,6 +48,9 @@ namespace trips {
 #endif
 constexpr int kChunk = TRIPS_CHUNK;         // (point, tile) pairs staged per K4 iteration
 constexpr int kPairsPerThread = kChunk / kTilePix;
+constexpr int kHashBits = 11;                 // pair hash of single-chunk tiles: load <= 1/2
+constexpr int kHash = 1 << kHashBits;
+static_assert(kHash >= 2 * kChunk, "pair hash sized for one chunk of pairs");
 constexpr int kPfUnroll = TRIPS_PF_UNROLL;      // bin pairs loaded together in k_raster phase F
 #ifndef TRIPS_BWD_SLOTS
 #define TRIPS_BWD_SLOTS 4
@@ -293,6 +299,17 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
     __shared__ uint32_t s_rej[kTilePix];             // fragments rejected by the threshold
     __shared__ uint64_t s_thr[kTilePix];             // per-pixel 16th smallest key so far
     __shared__ uint32_t s_warp[32];
+#if TRIPS_PAIR_HASH
+    // single-chunk tiles (M <= kChunk, nearly all of them): the chunk's pairs stay addressable by
+    // their bin position j -- key, origin code, kept-corner bits -- and a hash maps a point index
+    // to its pair, so the blend marks each kept fragment's pair directly (phase F without a second
+    // pass over the bin and without searching the pixels' lists)
+    __shared__ uint32_t s_hkey[kHash];
+    __shared__ uint16_t s_hval[kHash];
+    __shared__ uint64_t s_pkey[kChunk];
+    __shared__ uint16_t s_porig[kChunk];
+    __shared__ uint32_t s_pinfo[kChunk];
+#endif
 
     const int t = blockIdx.x;
     const TileCoord tc = tile_coord(P, t);
@@ -310,6 +327,11 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
     uint32_t total = 0;
 
     s_thr[tid] = kKeyMax;
+#if TRIPS_PAIR_HASH
+    const bool hashed = !COARSE && save && b1 - b0 <= (uint32_t)kChunk;
+    if (hashed)
+        for (int e = tid; e < kHash; e += kTilePix) s_hkey[e] = 0xffffffffu;   // visible after the chunk barrier
+#endif
     TRIPS_PCLK_START;
     // Chunks interleave the bin (chunk ch takes positions ch, ch + nch, ...): a pixel's
     // fragments then spread evenly over the chunks whatever the point order, which balances
@@ -338,6 +360,23 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
             pk[k] = j < m ? __ldg(reinterpret_cast<const unsigned long long*>(P.bin_key) + c0 + (size_t)j * nch) : 0ull;
             po[k] = j < m ? __ldg(P.bin_orig + c0 + (size_t)j * nch) : 0u;
         }
+#if TRIPS_PAIR_HASH
+        if (hashed) {                                // nch == 1: j is the pair's bin position
+#pragma unroll
+            for (int k = 0; k < kPairsPerThread; ++k) {
+                const int j = jl + k * kTilePix;
+                if (j < m) {
+                    s_pkey[j] = pk[k];
+                    s_porig[j] = (uint16_t)po[k];
+                    s_pinfo[j] = 0u;
+                    const uint32_t i = (uint32_t)pk[k];                   // a point has one pair per tile
+                    uint32_t h = (i * 2654435761u) >> (32 - kHashBits);
+                    while (atomicCAS(&s_hkey[h], 0xffffffffu, i) != 0xffffffffu) h = (h + 1) & (kHash - 1);
+                    s_hval[h] = (uint16_t)j;
+                }
+            }
+        }
+#endif
 #pragma unroll
         for (int k = 0; k < kPairsPerThread; ++k) {
 #pragma unroll
@@ -458,6 +497,7 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
     for (int b = 0; b < kCap / kBlendBatch; ++b) {
         if (b * kBlendBatch >= Keff || (!save && T == 0.f)) break;
         float4 rb[kBlendBatch][1 + FC / 4];
+        uint32_t rbi[kBlendBatch];
 #pragma unroll
         for (int u = 0; u < kBlendBatch; ++u) {
             const int mm = b * kBlendBatch + u;
@@ -466,6 +506,7 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
 #else
             const uint32_t ii = (uint32_t)s_kk[(mm < K ? mm : 0) * kTilePix + tid];
 #endif
+            rbi[u] = ii;
             gather_record<FC>(P, ii, rb[u]);
         }
 #pragma unroll
@@ -485,6 +526,15 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
                 A += tg;
                 T = __fmul_rn(T, __fsub_rn(1.0f, w.gamma));      // pinned: decides the T_min cut
                 if (save) P.kept_gamma[kidx + (size_t)mm * KS] = w.gamma;
+#if TRIPS_PAIR_HASH
+                if (hashed) {
+                    // this fragment is corner c = dx + 2 dy of its pair, kept at slot mm
+                    uint32_t h = (rbi[u] * 2654435761u) >> (32 - kHashBits);
+                    while (s_hkey[h] != rbi[u]) h = (h + 1) & (kHash - 1);
+                    const uint32_t c = (uint32_t)(w.dx + 2 * w.dy);
+                    atomicOr(&s_pinfo[s_hval[h]], (1u << (10 + c)) | ((uint32_t)mm << (14 + 4 * c)));
+                }
+#endif
                 if (TMIN && T < P.t_min) Keff = mm + 1;
             }
         }
@@ -516,6 +566,25 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
     uint64_t* s_kk = s_keys;                         // 16 x 256 keys (= kChunk * 4)
 #pragma unroll
     for (int mm = 0; mm < kCap; ++mm) s_kk[mm * kTilePix + tid] = r[mm];   // kKeyMax beyond K
+#endif
+#if TRIPS_PAIR_HASH
+    if (hashed) {
+        if (tid == 0) s_warp[0] = 0;
+        __syncthreads();                             // every kept fragment has marked its pair
+        const size_t kpb = kept_base(t);
+        for (uint32_t j = tid; j < M; j += kTilePix) {
+            const uint32_t kbits = s_pinfo[j];
+            if (kbits) {                             // bin order: the backward's gathers stay coherent
+                const uint32_t slot = atomicAdd(s_warp, 1u);
+                P.kp_key[kpb + slot] = s_pkey[j];
+                P.kp_info[kpb + slot] = kbits | (s_porig[j] & 0x3ffu);
+            }
+        }
+        __syncthreads();
+        if (tid == 0) P.kp_cnt[t] = s_warp[0];
+        TRIPS_PCLK(7);
+        return;
+    }
 #endif
     // per-pixel kept threshold: the Keff-th key (a key of this pixel is kept iff <= it)
     s_thr[tid] = Keff > 0 ? s_kk[(Keff - 1) * kTilePix + tid] : 0ull;
@@ -801,33 +870,51 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_BWD_CTAS) k_backward_pairs(Par
     __shared__ float s_c[kCap * kTilePix];           // [m][pixel] c_m, then dL/dgamma_m
     __shared__ float s_tg[kCap * kTilePix];          // [m][pixel] T_m gamma_m
     const int t = blockIdx.x;
-    const uint32_t npair = P.kp_cnt[t];
-    if (npair == 0) return;                          // uniform: nothing kept in this tile
-    const TileCoord tc = tile_coord(P, t);
+    const TileCoord tc = tile_coord(P, t);           // kernel parameters only: no memory round trip
     const LayerGeom& G = P.L[tc.l];
     const int tid = threadIdx.x;
     const int x_lo = tc.tx * kTile, y_lo = tc.ty * kTile;
     const int px = x_lo + (tid & (kTile - 1)), py = y_lo + (tid >> 4);
-    const int K = (int)(P.pix_meta[(size_t)t * kTilePix + tid] & 31u);
     const int64_t plane = (int64_t)G.W * G.H;
+    // the CTA's independent loads go out together (one memory round trip instead of three):
+    // the tile's kept-pair count, this pixel's kept-list length and its upstream gradient
+    const uint32_t npair = __ldg(P.kp_cnt + t);
+    const int K = (int)(__ldg(P.pix_meta + (size_t)t * kTilePix + tid) & 31u);
+    float gv[kGs ? FC : 1];
+    float gA = 0.f;
+    if (px < G.W && py < G.H) {
+        const float* gp = gpyr + G.float_off + (int64_t)py * G.W + px;
+        if constexpr (kGs) {
+#pragma unroll
+            for (int c = 0; c < FC; ++c) gv[c] = c < P.F ? __ldg(gp + c * plane) : 0.f;
+        }
+        gA = __ldg(gp + P.F * plane);
+    } else if constexpr (kGs) {
+#pragma unroll
+        for (int c = 0; c < FC; ++c) gv[c] = 0.f;
+    }
+    if (npair == 0) return;                          // uniform: nothing kept in this tile
     const float* gtile = gpyr + G.float_off + (int64_t)y_lo * G.W + x_lo;   // pixel q at (q & 15) + (q >> 4) W
     auto gC = [&](int f, int q) -> float {
         if constexpr (kGs) return s_g[f * kTilePix + q];
         else return f < P.F ? __ldg(gtile + f * plane + (int64_t)(q >> 4) * G.W + (q & (kTile - 1))) : 0.f;
     };
-    float gA = 0.f;
-    if (K > 0) {
-        const float* gp = gpyr + G.float_off + (int64_t)py * G.W + px;
-        if constexpr (kGs) {
+    if constexpr (kGs) {
 #pragma unroll
-            for (int c = 0; c < FC; ++c) s_g[c * kTilePix + tid] = c < P.F ? __ldg(gp + c * plane) : 0.f;
-        }
-        gA = __ldg(gp + P.F * plane);
+        for (int c = 0; c < FC; ++c) s_g[c * kTilePix + tid] = gv[c];
     }
-    __syncthreads();
     const size_t kpb = kept_base(t);
     const unsigned long long* kkey = reinterpret_cast<const unsigned long long*>(P.kp_key) + kpb;
     const uint32_t* kinfo = P.kp_info + kpb;
+    uint64_t rkey[kBwdSlots];
+    uint32_t rinfo[kBwdSlots];
+#pragma unroll
+    for (int u = 0; u < kBwdSlots; ++u) {            // issued before the barrier
+        const uint32_t j = tid + u * kTilePix;
+        rkey[u] = j < npair ? __ldg(kkey + j) : 0ull;
+        rinfo[u] = j < npair ? __ldg(kinfo + j) : 0u;            // no corner bits: inert
+    }
+    __syncthreads();
 
     // P1: c = <gC_q, tau_i> for every kept corner.  The first kBwdSlots pairs of each thread keep
     // their key, info and screen record in registers for P3 (all their loads are issued before
@@ -851,17 +938,9 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_BWD_CTAS) k_backward_pairs(Par
             }
         }
     };
-    uint64_t rkey[kBwdSlots];
-    uint32_t rinfo[kBwdSlots];
     float4 rgeo[kBwdSlots];
     {
         float4 rtau[kBwdSlots][FC / 4];
-#pragma unroll
-        for (int u = 0; u < kBwdSlots; ++u) {
-            const uint32_t j = tid + u * kTilePix;
-            rkey[u] = j < npair ? __ldg(kkey + j) : 0ull;
-            rinfo[u] = j < npair ? __ldg(kinfo + j) : 0u;            // no corner bits: inert
-        }
 #pragma unroll
         for (int u = 0; u < kBwdSlots; ++u) {
             const uint32_t i = (uint32_t)rkey[u];

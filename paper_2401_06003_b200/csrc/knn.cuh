@@ -29,7 +29,13 @@ namespace trips {
 constexpr int kKnnBits = 15;                  // quantisation steps per axis: 2^15
 constexpr int kKnnPasses = 6;                 // 45-bit codes + the non-finite marker's bit 47
 constexpr uint64_t kKnnNonFinite = (1ull << 48) - 1;
-constexpr int kKnnWin = 8;                    // sorted-order neighbours on each side for the bound
+#ifndef TRIPS_KNN_UNION
+#define TRIPS_KNN_UNION 6          // warp mode when the union box is <= this x the largest lane box (+64 steps)
+#endif
+#ifndef TRIPS_KNN_WIN
+#define TRIPS_KNN_WIN 8
+#endif
+constexpr int kKnnWin = TRIPS_KNN_WIN;                    // sorted-order neighbours on each side for the bound
 
 struct KnnWs {
     using Key = uint64_t;
@@ -277,7 +283,7 @@ __global__ void __launch_bounds__(256) k_knn_query(KnnWs W, float* __restrict__ 
             uext = max(uext, uhi[a] - ulo[a]);
         }
         lext = __reduce_max_sync(kAll, need ? lext : 0);
-        if (uext <= 3 * lext + 64) {
+        if (uext <= TRIPS_KNN_UNION * lext + 64) {
             // the union box is covered by <= 3 x 3 x 3 aligned octree cells of the smallest size that
             // spans it in 3; each cell is one contiguous code range of the sorted array, located by a
             // lane of its own (parallel lower_bounds); the warp then sweeps the cells' ranges 32
