@@ -45,7 +45,18 @@ constexpr int kDecBBytes = kDecN * kDecXC * 2;          // 12 KB per tap
 constexpr int kDecEpiWarps = 8;                         // 2 per TMEM lane quarter (16 channels each)
 constexpr int kDecThreads = 64 + 32 * kDecEpiWarps;     // TMA warp, MMA warp, epilogue warps
 constexpr int kDecMaxOut = 32;
-constexpr int kDecSmem = 1024 + kDecTaps * kDecBBytes + kDecStages * kDecABytes + 256;
+#ifndef TRIPS_DEC_ROWS
+#define TRIPS_DEC_ROWS 1           // 1: row boxes reused across taps and tiles; 0: one box per tap
+#endif
+#ifndef TRIPS_DEC_BO
+#define TRIPS_DEC_BO 0             // descriptor base_offset for row-shifted operands (0 or the address phase)
+#endif
+constexpr int kDecRowPix = kDecM + 2;                   // a row box: the tile's 128 pixels + 1 halo each side
+constexpr int kDecRowBytes = kDecRowPix * kDecXC * 2;   // 16640 B written by the TMA
+constexpr int kDecRowSlot = 17 * 1024;                  // slots 1024-B aligned (swizzle phase)
+constexpr int kDecRowSlots = 4;                         // rows y-1, y, y+1 in use + the next one loading
+constexpr int kDecSmem = TRIPS_DEC_ROWS ? 1024 + kDecTaps * kDecBBytes + kDecRowSlots * kDecRowSlot + 256
+                                        : 1024 + kDecTaps * kDecBBytes + kDecStages * kDecABytes + 256;
 
 // ----------------------------------------------------------------------------- PTX wrappers
 
@@ -87,7 +98,11 @@ __device__ __forceinline__ void dec_tc_fence_after() { asm volatile("tcgen05.fen
 // K-major), SBO = 1024 B >> 4, version 1 (sm_100), layout SWIZZLE_128B (2).
 __device__ __forceinline__ uint64_t dec_desc(uint32_t saddr)
 {
-    return (uint64_t)((saddr >> 4) & 0x3fffu) | (1ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
+    uint64_t d = (uint64_t)((saddr >> 4) & 0x3fffu) | (1ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
+#if TRIPS_DEC_BO
+    d |= (uint64_t)((saddr >> 7) & 7u) << 49;        // start not on a 1024-B swizzle repeat: its phase
+#endif
+    return d;
 }
 // instruction descriptor, kind::f16: D f32 (bits 4-5 = 1), A = B = f16 (0), both K-major,
 // N >> 3 at bits 17-22, M >> 4 at bits 24-28
@@ -250,23 +265,40 @@ __global__ void __launch_bounds__(kDecThreads, 1) k_dec_conv(const __grid_consta
     extern __shared__ __align__(1024) uint8_t dec_smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dec_smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sB = smem;                                           // 9 x 12 KB
-    uint8_t* sA = smem + kDecTaps * kDecBBytes;                   // stages x 16 KB
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sA + kDecStages * kDecABytes);
+    uint8_t* sA = smem + kDecTaps * kDecBBytes;                   // tap stages x 16 KB | row slots x 17 KB
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sA + (TRIPS_DEC_ROWS ? kDecRowSlots * kDecRowSlot : kDecStages * kDecABytes));
     uint64_t* full = bars;                                        // [stages]
     uint64_t* empty = bars + kDecStages;                          // [stages]
     uint64_t* tfull = bars + 2 * kDecStages;                      // [2]
     uint64_t* tempty = tfull + 2;                                 // [2]
     uint64_t* bbar = tempty + 2;                                  // weights loaded
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bbar + 1);
+    uint64_t* mdone = bbar + 1;                                   // [2] MMAs of tile parity p finished
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mdone + 2);
 
     const DecLayer& L = D.L[l];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int xt = (L.W + kDecM - 1) / kDecM;
     const int ntiles = L.H * xt;
+#if TRIPS_DEC_ROWS
+    // each CTA takes a contiguous run of the column-segment-major tile order: consecutive rows of
+    // one 128-pixel column, so the row boxes y, y + 1 of a tile are rows of the next one too
+    const int per = (ntiles + gridDim.x - 1) / gridDim.x;
+    const int tile0 = blockIdx.x * per, tile1 = min(ntiles, tile0 + per), tstep = 1;
+    auto tile_y = [&](int tile) { return tile % L.H; };
+    auto tile_x0 = [&](int tile) { return (tile / L.H) * kDecM; };
+#else
+    const int tile0 = blockIdx.x, tile1 = ntiles, tstep = gridDim.x;
+    auto tile_y = [&](int tile) { return tile / xt; };
+    auto tile_x0 = [&](int tile) { return (tile % xt) * kDecM; };
+#endif
 
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < kDecStages; ++s) { dec_mbar_init(full + s, 1); dec_mbar_init(empty + s, 1); }
-        for (int a = 0; a < 2; ++a) { dec_mbar_init(tfull + a, 1); dec_mbar_init(tempty + a, kDecEpiWarps); }
+        for (int a = 0; a < 2; ++a) {
+            dec_mbar_init(tfull + a, 1);
+            dec_mbar_init(tempty + a, kDecEpiWarps);
+            dec_mbar_init(mdone + a, 1);
+        }
         dec_mbar_init(bbar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -285,10 +317,36 @@ __global__ void __launch_bounds__(kDecThreads, 1) k_dec_conv(const __grid_consta
             // ---- TMA producer: the weights once, then the 9 shifted A boxes of every tile
             dec_mbar_expect_tx(bbar, kDecTaps * kDecBBytes);
             for (int t = 0; t < kDecTaps; ++t) dec_tma_2d(sB + t * kDecBBytes, &tmB, bbar, 0, (l * kDecTaps + t) * kDecN);
+#if TRIPS_DEC_ROWS
+            // row boxes {64 ch, 130 px, 1 row} at (x0 - 1, r) in slot r & 3; a slot is reloaded once
+            // the MMAs of the last tile that read it have finished
+            int skey[kDecRowSlots], slast[kDecRowSlots];
+#pragma unroll
+            for (int q = 0; q < kDecRowSlots; ++q) { skey[q] = -1; slast[q] = -1; }
+            int it = 0;
+            for (int tile = tile0; tile < tile1; tile += tstep, ++it) {
+                const int y = tile_y(tile), x0 = tile_x0(tile);
+#pragma unroll
+                for (int dy = -1; dy <= 1; ++dy) {
+                    const int r = y + dy, sl = r & (kDecRowSlots - 1);
+                    const int key = (x0 / kDecM) * (L.H + 2) + (r + 1);
+                    if (skey[sl] != key) {
+                        if (slast[sl] >= 0) {
+                            const int w = max(slast[sl], it - 2);       // MMAs complete in issue order
+                            dec_mbar_wait(mdone + (w & 1), (uint32_t)(w >> 1) & 1u);
+                        }
+                        dec_mbar_expect_tx(full + sl, kDecRowBytes);
+                        dec_tma_3d(sA + sl * kDecRowSlot, &tmX, full + sl, 0, x0 - 1, r);
+                        skey[sl] = key;
+                    }
+                    slast[sl] = it;
+                }
+            }
+#else
             int s = 0;
             uint32_t ph = 0;
-            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-                const int y = tile / xt, x0 = (tile % xt) * kDecM;
+            for (int tile = tile0; tile < tile1; tile += tstep) {
+                const int y = tile_y(tile), x0 = tile_x0(tile);
                 for (int t = 0; t < kDecTaps; ++t) {
                     dec_mbar_wait(empty + s, ph ^ 1);
                     dec_mbar_expect_tx(full + s, kDecABytes);
@@ -296,15 +354,53 @@ __global__ void __launch_bounds__(kDecThreads, 1) k_dec_conv(const __grid_consta
                     if (++s == kDecStages) { s = 0; ph ^= 1; }
                 }
             }
+#endif
         }
     } else if (warp == 1) {
         if (lane == 0) {
             // ---- MMA issuer
             dec_mbar_wait(bbar, 0);
+#if TRIPS_DEC_ROWS
+            int skey[kDecRowSlots];
+            uint32_t snl[kDecRowSlots];
+#pragma unroll
+            for (int q = 0; q < kDecRowSlots; ++q) { skey[q] = -1; snl[q] = 0; }
+            int it = 0;
+            for (int tile = tile0; tile < tile1; tile += tstep, ++it) {
+                const int acc = it & 1;
+                const uint32_t aph = (uint32_t)(it >> 1) & 1u;
+                const int y = tile_y(tile), x0 = tile_x0(tile);
+                dec_mbar_wait(tempty + acc, aph ^ 1);
+                uint32_t rowa[3];
+#pragma unroll
+                for (int dy = -1; dy <= 1; ++dy) {            // the producer's slot bookkeeping, replayed
+                    const int r = y + dy, sl = r & (kDecRowSlots - 1);
+                    const int key = (x0 / kDecM) * (L.H + 2) + (r + 1);
+                    if (skey[sl] != key) {
+                        skey[sl] = key;
+                        dec_mbar_wait(full + sl, snl[sl] & 1u);
+                        ++snl[sl];
+                    }
+                    rowa[dy + 1] = dec_smem_u32(sA + sl * kDecRowSlot);
+                }
+                dec_tc_fence_after();
+                const uint32_t d = tmem + (uint32_t)(acc * kDecN);
+#pragma unroll
+                for (int t = 0; t < kDecTaps; ++t) {
+                    // tap (dy, dx): the row box of y + dy from pixel dx + 1 on (one 128-B row per pixel)
+                    const uint32_t a0 = rowa[t / 3] + 128u * (uint32_t)(t % 3), b0 = dec_smem_u32(sB + t * kDecBBytes);
+#pragma unroll
+                    for (int k = 0; k < kDecXC / 16; ++k)
+                        dec_umma(d, dec_desc(a0 + 32 * k), dec_desc(b0 + 32 * k), (t | k) ? 1u : 0u);
+                }
+                dec_umma_commit(mdone + acc);                 // row slots read by this tile may be reused
+                dec_umma_commit(tfull + acc);                 // accumulator ready for the epilogue
+            }
+#else
             int s = 0;
             uint32_t ph = 0;
             int it = 0;
-            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+            for (int tile = tile0; tile < tile1; tile += tstep, ++it) {
                 const int acc = it & 1;
                 const uint32_t aph = (uint32_t)(it >> 1) & 1u;
                 dec_mbar_wait(tempty + acc, aph ^ 1);
@@ -322,6 +418,7 @@ __global__ void __launch_bounds__(kDecThreads, 1) k_dec_conv(const __grid_consta
                 }
                 dec_umma_commit(tfull + acc);                 // accumulator ready for the epilogue
             }
+#endif
         }
     } else {
         // ---- epilogue warps 2-9: TMEM lane quarter q = warp % 4 (tile rows 32 q ..), channel half
@@ -334,12 +431,12 @@ __global__ void __launch_bounds__(kDecThreads, 1) k_dec_conv(const __grid_consta
         const bool last = l == 0;
         float* Yo = D.Y[l & 1];
         int it = 0;
-        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+        for (int tile = tile0; tile < tile1; tile += tstep, ++it) {
             const int acc = it & 1;
             const uint32_t aph = (uint32_t)(it >> 1) & 1u;
             dec_mbar_wait(tfull + acc, aph);
             dec_tc_fence_after();
-            const int y = tile / xt, x = (tile % xt) * kDecM + 32 * q + lane;
+            const int y = tile_y(tile), x = tile_x0(tile) + 32 * q + lane;
             const int64_t p = (int64_t)y * L.W + x;
             const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * kDecN);
             if (!last) {

@@ -750,7 +750,7 @@ int trips_decode(const trips_plan* p, void* dws, const float* params, int32_t ou
         CUtensorMap tmX;
         const cuuint64_t dims[3] = {(cuuint64_t)kDecXC, (cuuint64_t)L.W, (cuuint64_t)L.H};
         const cuuint64_t strides[2] = {(cuuint64_t)kDecXC * 2, (cuuint64_t)L.W * kDecXC * 2};
-        const cuuint32_t box[3] = {(cuuint32_t)kDecXC, (cuuint32_t)kDecM, 1};
+        const cuuint32_t box[3] = {(cuuint32_t)kDecXC, (cuuint32_t)(TRIPS_DEC_ROWS ? kDecRowPix : kDecM), 1};
         const cuuint32_t estr[3] = {1, 1, 1};
         if (encode(&tmX, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, D.X, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
