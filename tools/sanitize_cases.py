@@ -2,7 +2,8 @@
 """Small cases for compute-sanitizer (memcheck / racecheck / synccheck / initcheck): C1, the
 adversarial scene and a dense-tile scene (several chunks, lists >> 16), each through project ->
 forward (saved) -> backward (+ camera gradient) -> SCREEN_GRADS export, plus the T_min and
-coarse-layer variants and the kNN / Morton utilities.
+coarse-layer variants, the kNN / Morton utilities (incl. a clustered, duplicate-heavy cloud: both
+kNN query modes) and the gated-conv decoder (TMA + tcgen05; odd sizes, 1 and 3 layers).
 
   compute-sanitizer --tool racecheck python tools/sanitize_cases.py
 """
@@ -13,7 +14,7 @@ import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2401_06003_b200 import Rasterizer, knn_sizes, morton_order  # noqa: E402
+from paper_2401_06003_b200 import Decoder, Rasterizer, knn_sizes, morton_order  # noqa: E402
 from synth import scenes  # noqa: E402
 
 dev = torch.device("cuda:0")
@@ -37,5 +38,15 @@ for name, sc, kw in cases:
 pos = T(scenes.c1(n=5000).pos)
 knn_sizes(pos)
 morton_order(pos)
+rng = np.random.default_rng(5)
+cl = np.concatenate([rng.normal(size=(400, 3)) * 1e-3 + rng.uniform(-5, 5, 3) for _ in range(5)] +
+                    [np.repeat([[0.5, 0.5, 0.5]], 300, 0), [[np.nan, 0, 0]]]).astype(np.float32)
+knn_sizes(T(cl))
+for (W, H, n, F) in ((100, 77, 3, 4), (130, 40, 1, 8)):
+    r = Rasterizer(W, H, n, F, max_points=16, device=dev)
+    dec = Decoder(r, 3)
+    prm = torch.randn(dec.param_count, device=dev) * 0.1
+    out = dec(prm, torch.randn(r.pyramid_floats, device=dev))
+    print("decoder", W, H, n, F, float(out.abs().sum()), flush=True)
 torch.cuda.synchronize()
 print("sanitize cases done")
