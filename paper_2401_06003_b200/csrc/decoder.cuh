@@ -144,6 +144,8 @@ struct DecLayer {
 
 struct DecParams {
     int32_t n_layers, F, out_ch;
+    int32_t xc;                    // X channels stored: 48 when F + 1 <= 16, else 64 (TMA reads 64, the
+                                   // channels beyond xc come back zero-filled and their K steps are skipped)
     DecLayer L[16];
     int64_t prm_out;               // float offset of Wo [out][32], bo [out]
     const float* prm;              // flat fp32 parameters (oracle/decoder.py param_layout)
@@ -204,9 +206,10 @@ __global__ void __launch_bounds__(256) k_dec_prep(DecParams D, int l)
         }
         __syncthreads();
     }
-    for (int it = threadIdx.x; it < kPrepW * kPrepH * (kDecXC / 8); it += blockDim.x) {
-        const int grp = it & (kDecXC / 8 - 1);
-        const int q = it >> 3;
+    const int ng = D.xc / 8;                         // 16-byte channel groups per pixel
+    for (int it = threadIdx.x; it < kPrepW * kPrepH * ng; it += blockDim.x) {
+        const int q = it / ng;
+        const int grp = it - q * ng;
         const int y = y0 + q / kPrepW, x = x0 + (q & (kPrepW - 1));
         if (y >= L.H || x >= L.W) continue;
         const int p = y * L.W + x;
@@ -248,7 +251,7 @@ __global__ void __launch_bounds__(256) k_dec_prep(DecParams D, int l)
         __half2 h2[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) h2[j] = __floats2half2_rn(v[2 * j], v[2 * j + 1]);
-        *reinterpret_cast<uint4*>(D.X + (int64_t)p * kDecXC + grp * 8) = *reinterpret_cast<uint4*>(h2);
+        *reinterpret_cast<uint4*>(D.X + (int64_t)p * D.xc + grp * 8) = *reinterpret_cast<uint4*>(h2);
     }
 }
 
@@ -391,7 +394,7 @@ __global__ void __launch_bounds__(kDecThreads, 1) k_dec_conv(const __grid_consta
                     const uint32_t a0 = rowa[t / 3] + 128u * (uint32_t)(t % 3), b0 = dec_smem_u32(sB + t * kDecBBytes);
 #pragma unroll
                     for (int k = 0; k < kDecXC / 16; ++k)
-                        dec_umma(d, dec_desc(a0 + 32 * k), dec_desc(b0 + 32 * k), (t | k) ? 1u : 0u);
+                        if (16 * k < D.xc) dec_umma(d, dec_desc(a0 + 32 * k), dec_desc(b0 + 32 * k), (t | k) ? 1u : 0u);
                 }
                 dec_umma_commit(mdone + acc);                 // row slots read by this tile may be reused
                 dec_umma_commit(tfull + acc);                 // accumulator ready for the epilogue
@@ -412,7 +415,7 @@ __global__ void __launch_bounds__(kDecThreads, 1) k_dec_conv(const __grid_consta
                     const uint32_t a0 = dec_smem_u32(sA + s * kDecABytes), b0 = dec_smem_u32(sB + t * kDecBBytes);
 #pragma unroll
                     for (int k = 0; k < kDecXC / 16; ++k)    // K16 steps: +32 B inside the swizzle atom
-                        dec_umma(d, dec_desc(a0 + 32 * k), dec_desc(b0 + 32 * k), (t | k) ? 1u : 0u);
+                        if (16 * k < D.xc) dec_umma(d, dec_desc(a0 + 32 * k), dec_desc(b0 + 32 * k), (t | k) ? 1u : 0u);
                     dec_umma_commit(empty + s);               // smem slot free once these MMAs finish
                     if (++s == kDecStages) { s = 0; ph ^= 1; }
                 }

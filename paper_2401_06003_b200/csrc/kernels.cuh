@@ -61,6 +61,10 @@ constexpr int kBwdSlots = TRIPS_BWD_SLOTS;      // kept pairs per thread held in
 #endif
 constexpr int kBatch = TRIPS_BWD_BATCH;     // record gathers issued together (memory-level parallelism)
 constexpr int kBlendBatch = TRIPS_BLEND_BATCH;  // same in k_raster's blend (register budget: 3 CTAs/SM)
+// wide descriptors hold FC / 4 float4 per gathered record: fewer records in flight keeps them in
+// registers (F > 8 spilled kilobytes per thread at the F = 4 batch sizes)
+template <int FC> __host__ __device__ constexpr int blend_batch() { return FC <= 8 ? kBlendBatch : (FC <= 16 ? 2 : 1); }
+template <int FC> __host__ __device__ constexpr int bwd_slots() { return FC <= 8 ? kBwdSlots : (FC <= 16 ? 2 : 1); }
 
 // Experiment builds only (-DTRIPS_PHASE_CLOCK): per-phase clock64 accumulation of k_raster
 // (thread 0 of each CTA, after a barrier), read with trips_debug_phase_clocks().
@@ -494,13 +498,14 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
     // the fragment after which the fp32 transmittance drops below t_min
     int Keff = K;
 #pragma unroll
-    for (int b = 0; b < kCap / kBlendBatch; ++b) {
-        if (b * kBlendBatch >= Keff || (!save && T == 0.f)) break;
-        float4 rb[kBlendBatch][1 + FC / 4];
-        uint32_t rbi[kBlendBatch];
+    constexpr int kBB = blend_batch<FC>();
+    for (int b = 0; b < kCap / kBB; ++b) {
+        if (b * kBB >= Keff || (!save && T == 0.f)) break;
+        float4 rb[kBB][1 + FC / 4];
+        uint32_t rbi[kBB];
 #pragma unroll
-        for (int u = 0; u < kBlendBatch; ++u) {
-            const int mm = b * kBlendBatch + u;
+        for (int u = 0; u < kBB; ++u) {
+            const int mm = b * kBB + u;
 #if TRIPS_BLEND_REG
             const uint32_t ii = (uint32_t)(mm < K ? r[mm] : r[0]);
 #else
@@ -510,8 +515,8 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
             gather_record<FC>(P, ii, rb[u]);
         }
 #pragma unroll
-        for (int u = 0; u < kBlendBatch; ++u) {
-            const int mm = b * kBlendBatch + u;
+        for (int u = 0; u < kBB; ++u) {
+            const int mm = b * kBB + u;
             if (mm < Keff) {
                 const FragW w = frag_weights(rb[u][0], tc.l, P.n_layers, px, py);
                 const float tg = T * w.gamma;
@@ -696,18 +701,19 @@ __global__ void __launch_bounds__(kTilePix) k_coarse_blend(Params P, float* __re
     float A = 0.f, T = 1.f;
     int Keff = K;
 #pragma unroll
-    for (int b = 0; b < kCap / kBlendBatch; ++b) {
-        if (b * kBlendBatch >= Keff || (!save && T == 0.f)) break;
-        float4 rb[kBlendBatch][1 + FC / 4];
+    constexpr int kBB = blend_batch<FC>();
+    for (int b = 0; b < kCap / kBB; ++b) {
+        if (b * kBB >= Keff || (!save && T == 0.f)) break;
+        float4 rb[kBB][1 + FC / 4];
 #pragma unroll
-        for (int u = 0; u < kBlendBatch; ++u) {
-            const int mm = b * kBlendBatch + u;
+        for (int u = 0; u < kBB; ++u) {
+            const int mm = b * kBB + u;
             const uint32_t ii = (uint32_t)(mm < K ? r[mm] : r[0]) >> 4;
             gather_record<FC>(P, ii, rb[u]);
         }
 #pragma unroll
-        for (int u = 0; u < kBlendBatch; ++u) {
-            const int mm = b * kBlendBatch + u;
+        for (int u = 0; u < kBB; ++u) {
+            const int mm = b * kBB + u;
             if (mm < Keff) {
                 const int d = (int)(r[mm] & 15u);
                 const FragW w = frag_weights(rb[u][0], tc.l + d, P.n_layers, px >> d, py >> d);
@@ -906,19 +912,20 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_BWD_CTAS) k_backward_pairs(Par
     const size_t kpb = kept_base(t);
     const unsigned long long* kkey = reinterpret_cast<const unsigned long long*>(P.kp_key) + kpb;
     const uint32_t* kinfo = P.kp_info + kpb;
-    uint64_t rkey[kBwdSlots];
-    uint32_t rinfo[kBwdSlots];
+    constexpr int kBS = bwd_slots<FC>();
+    uint64_t rkey[kBS];
+    uint32_t rinfo[kBS];
 #pragma unroll
-    for (int u = 0; u < kBwdSlots; ++u) {            // issued before the barrier
+    for (int u = 0; u < kBS; ++u) {            // issued before the barrier
         const uint32_t j = tid + u * kTilePix;
         rkey[u] = j < npair ? __ldg(kkey + j) : 0ull;
         rinfo[u] = j < npair ? __ldg(kinfo + j) : 0u;            // no corner bits: inert
     }
     __syncthreads();
 
-    // P1: c = <gC_q, tau_i> for every kept corner.  The first kBwdSlots pairs of each thread keep
+    // P1: c = <gC_q, tau_i> for every kept corner.  The first kBS pairs of each thread keep
     // their key, info and screen record in registers for P3 (all their loads are issued before
-    // the first use); pairs beyond kBwdSlots * 256 (dense tiles) are re-read in P3.
+    // the first use); pairs beyond kBS * 256 (dense tiles) are re-read in P3.
     auto corners_c = [&](uint32_t info, const float4 (&tb)[FC / 4]) {
         const int q0 = (int)(info & 31u) - 1 + ((int)((info >> 5) & 31u) - 1) * kTile;
 #pragma unroll
@@ -938,11 +945,11 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_BWD_CTAS) k_backward_pairs(Par
             }
         }
     };
-    float4 rgeo[kBwdSlots];
+    float4 rgeo[kBS];
     {
-        float4 rtau[kBwdSlots][FC / 4];
+        float4 rtau[kBS][FC / 4];
 #pragma unroll
-        for (int u = 0; u < kBwdSlots; ++u) {
+        for (int u = 0; u < kBS; ++u) {
             const uint32_t i = (uint32_t)rkey[u];
             if (rinfo[u]) {
                 const float4* tp = reinterpret_cast<const float4*>(P.tau + (size_t)i * FC);
@@ -952,10 +959,10 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_BWD_CTAS) k_backward_pairs(Par
             }
         }
 #pragma unroll
-        for (int u = 0; u < kBwdSlots; ++u)
+        for (int u = 0; u < kBS; ++u)
             if (rinfo[u]) corners_c(rinfo[u], rtau[u]);
     }
-    for (uint32_t j = tid + kBwdSlots * kTilePix; j < npair; j += kTilePix) {
+    for (uint32_t j = tid + kBS * kTilePix; j < npair; j += kTilePix) {
         const uint32_t i = (uint32_t)__ldg(kkey + j);
         const uint32_t info = __ldg(kinfo + j);
         float4 tb[FC / 4];
@@ -1035,9 +1042,9 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_BWD_CTAS) k_backward_pairs(Par
         point_reduce<FC, CAM, SCREEN>(P, i, r0, z, gxs, gys, gs, galpha, gt, go, cg);
     };
 #pragma unroll
-    for (int u = 0; u < kBwdSlots; ++u)
+    for (int u = 0; u < kBS; ++u)
         if (rinfo[u]) pair_chain(rkey[u], rinfo[u], rgeo[u]);
-    for (uint32_t j = tid + kBwdSlots * kTilePix; j < npair; j += kTilePix) {
+    for (uint32_t j = tid + kBS * kTilePix; j < npair; j += kTilePix) {
         const uint64_t key = __ldg(kkey + j);
         pair_chain(key, __ldg(kinfo + j), __ldg(P.geo + (uint32_t)key));
     }

@@ -691,6 +691,7 @@ int trips_decode(const trips_plan* p, void* dws, const float* params, int32_t ou
     D.n_layers = p->n_layers;
     D.F = p->F;
     D.out_ch = out_channels;
+    D.xc = (p->F + 1 <= 16) ? 48 : kDecXC;
     int64_t o = 0;
     for (int l = 0; l < p->n_layers; ++l) {
         DecLayer& L = D.L[l];
@@ -748,8 +749,8 @@ int trips_decode(const trips_plan* p, void* dws, const float* params, int32_t ou
         k_dec_prep<<<dim3((L.W + kPrepW - 1) / kPrepW, (L.H + kPrepH - 1) / kPrepH), 256, 0, st>>>(D, l);
         if ((rc = check_launch())) return rc;
         CUtensorMap tmX;
-        const cuuint64_t dims[3] = {(cuuint64_t)kDecXC, (cuuint64_t)L.W, (cuuint64_t)L.H};
-        const cuuint64_t strides[2] = {(cuuint64_t)kDecXC * 2, (cuuint64_t)L.W * kDecXC * 2};
+        const cuuint64_t dims[3] = {(cuuint64_t)D.xc, (cuuint64_t)L.W, (cuuint64_t)L.H};
+        const cuuint64_t strides[2] = {(cuuint64_t)D.xc * 2, (cuuint64_t)L.W * D.xc * 2};
         const cuuint32_t box[3] = {(cuuint32_t)kDecXC, (cuuint32_t)(TRIPS_DEC_ROWS ? kDecRowPix : kDecM), 1};
         const cuuint32_t estr[3] = {1, 1, 1};
         if (encode(&tmX, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, D.X, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
