@@ -117,9 +117,13 @@ typedef enum {
 
 /* ---- plan ------------------------------------------------------------------------- */
 
-/* Creates a plan for images of width x height and up to max_points points.
+/* Creates a plan for images of width x height and up to max_points points.  Plans whose pyramid
+ * has more 16 x 16 tiles than the binning kernels' shared-memory counters hold (49 152, e.g. 8K
+ * frames) bin with global-memory counters instead (same results; slower binning); setting the
+ * environment variable TRIPS_FORCE_GLOBAL_BINNING=1 before creating a plan selects that path
+ * at any size (tests).
  * Errors: TRIPS_ERR_ARG (null, bad config, width/height < 1 or > 32768, max_points < 0 or
- * >= 2^28). */
+ * >= 2^28, more than 2^20 tiles). */
 int trips_plan_create(const trips_config* cfg, int32_t width, int32_t height, int64_t max_points,
                       trips_plan** out);
 void trips_plan_destroy(trips_plan* plan);

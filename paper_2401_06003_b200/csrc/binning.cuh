@@ -112,13 +112,17 @@ __device__ __forceinline__ void scan_tile_totals(const Params& P, uint32_t* s_to
 
 // Projects every point once (exact block), writes its screen record and depth, and counts its
 // (point, tile) pairs in shared-memory counters.
-template <int FC>
+// GLOBAL (plans with more tiles than the shared-memory counters hold, T > kMaxTilesSmem, e.g.
+// 8K frames): one global atomic per pair on the tile total instead; the host scans the totals
+// (k_gscan_*) and k_emit<true> places pairs with global cursors.
+template <int FC, bool GLOBAL>
 __global__ void __launch_bounds__(kBinThreads, kBinCtasPerSm) k_count(Params P, int8_t* __restrict__ level_out,
                                                        float* __restrict__ proj_out)
 {
-    extern __shared__ __align__(16) uint32_t s_hist[];            // [T]
+    extern __shared__ __align__(16) uint32_t s_hist[];            // [T] (GLOBAL: unused)
     __shared__ uint32_t s_v;
-    for (int t = threadIdx.x; t < P.T; t += blockDim.x) s_hist[t] = 0;
+    if (!GLOBAL)
+        for (int t = threadIdx.x; t < P.T; t += blockDim.x) s_hist[t] = 0;
     if (threadIdx.x == 0) s_v = 0;
     __syncthreads();
     int b, e;
@@ -189,13 +193,18 @@ __global__ void __launch_bounds__(kBinThreads, kBinCtasPerSm) k_count(Params P, 
         }
         if (vis) {
             ++nvis;
-            for_each_pair(P, xs, ys, s, [&](int t, uint32_t) { atomicAdd(&s_hist[t], 1u); });
+            if (GLOBAL) for_each_pair(P, xs, ys, s, [&](int t, uint32_t) { atomicAdd(&P.tile_cnt[t], 1u); });
+            else for_each_pair(P, xs, ys, s, [&](int t, uint32_t) { atomicAdd(&s_hist[t], 1u); });
         }
       }
     }
     const uint32_t wv = __reduce_add_sync(0xffffffffu, nvis);
     if (lane_id() == 0 && wv) atomicAdd(&s_v, wv);
     __syncthreads();
+    if constexpr (GLOBAL) {
+        if (threadIdx.x == 0) P.cta_vis[blockIdx.x] = s_v;
+        return;
+    }
     // reserve this CTA's slice of every tile it touches: tile_cnt[t] holds the running tile
     // total here (k_tscan turns totals into offsets); the returned value is the CTA's offset
     // inside the tile.  One atomic per (CTA, non-empty tile), spread over T addresses; every
@@ -266,13 +275,67 @@ __global__ void __launch_bounds__(1024) k_tscan(Params P)
     if (threadIdx.x == 0) P.tile_off[T] = ta;
 }
 
+// --------------------------------------------------------------------------- k_gscan_*
+
+// tile_off <- exclusive scan of tile_cnt[0..T) in global memory (GLOBAL binning), in three
+// launches: 1024-entry segments, their totals (one CTA), offsets added; tile_off[T] = total.
+__global__ void __launch_bounds__(1024) k_gscan_seg(Params P, uint32_t* bsum)
+{
+    __shared__ uint32_t ws[32];
+    const int t = blockIdx.x * 1024 + threadIdx.x;
+    const uint32_t v = t < P.T ? P.tile_cnt[t] : 0u;
+    uint32_t tot;
+    const uint32_t ex = block_excl_scan(v, ws, &tot);
+    if (t < P.T) P.tile_off[t] = ex;
+    if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(1024) k_gscan_top(Params P, uint32_t* bsum)
+{
+    __shared__ uint32_t ws[32];
+    const int nseg = (P.T + 1023) / 1024;
+    uint32_t carry = 0;
+    for (int base = 0; base < nseg; base += 1024) {
+        const int e = base + threadIdx.x;
+        const uint32_t v = e < nseg ? bsum[e] : 0u;
+        uint32_t tot;
+        const uint32_t ex = block_excl_scan(v, ws, &tot);
+        if (e < nseg) bsum[e] = carry + ex;
+        carry += tot;
+    }
+    if (threadIdx.x == 0) P.tile_off[P.T] = carry;
+}
+
+__global__ void __launch_bounds__(1024) k_gscan_add(Params P, const uint32_t* bsum)
+{
+    const int t = blockIdx.x * 1024 + threadIdx.x;
+    if (t < P.T) P.tile_off[t] += bsum[blockIdx.x];
+}
+
 // --------------------------------------------------------------------------- k_emit
 
 // Same point partition as k_count: re-enumerates each visible point's pairs from its screen
 // record (no projection) and places them at tile_off[t] + this CTA's slice + shared cursor.
+template <bool GLOBAL>
 __global__ void __launch_bounds__(kBinThreads, kBinCtasPerSm) k_emit(Params P)
 {
     extern __shared__ __align__(16) uint32_t s_cur[];             // [T] fill cursors
+    if constexpr (GLOBAL) {
+        // tile_cnt was re-zeroed after the scan: it is the per-tile fill cursor
+        int b, e;
+        cta_range(P.n, b, e);
+        for (int i = b + threadIdx.x; i < e; i += blockDim.x) {
+            const float4 r0 = __ldg(P.geo + i);
+            if (!(r0.z >= 0.f)) continue;                         // culled
+            const uint64_t key = ((uint64_t)__float_as_uint(__ldg(P.zbuf + i)) << 32) | (uint32_t)i;
+            for_each_pair(P, r0.x, r0.y, r0.z, [&](int t, uint32_t o) {
+                const uint32_t pos = P.tile_off[t] + atomicAdd(&P.tile_cnt[t], 1u);
+                P.bin_key[pos] = key;
+                P.bin_orig[pos] = (uint16_t)o;
+            });
+        }
+        return;
+    }
     const uint32_t* row = P.hist + (size_t)blockIdx.x * P.T;
 #if TRIPS_EMIT_SCAN
     // every CTA scans the tile totals itself (T independent coalesced loads, one block scan):

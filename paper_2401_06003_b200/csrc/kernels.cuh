@@ -497,8 +497,8 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
     // T_min variant (0 = the exact definition): the kept list ends with
     // the fragment after which the fp32 transmittance drops below t_min
     int Keff = K;
-#pragma unroll
     constexpr int kBB = blend_batch<FC>();
+#pragma unroll
     for (int b = 0; b < kCap / kBB; ++b) {
         if (b * kBB >= Keff || (!save && T == 0.f)) break;
         float4 rb[kBB][1 + FC / 4];
@@ -700,8 +700,8 @@ __global__ void __launch_bounds__(kTilePix) k_coarse_blend(Params P, float* __re
     for (int c = 0; c < FC; ++c) C[c] = 0.f;
     float A = 0.f, T = 1.f;
     int Keff = K;
-#pragma unroll
     constexpr int kBB = blend_batch<FC>();
+#pragma unroll
     for (int b = 0; b < kCap / kBB; ++b) {
         if (b * kBB >= Keff || (!save && T == 0.f)) break;
         float4 rb[kBB][1 + FC / 4];

@@ -6,6 +6,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -45,6 +46,8 @@ struct trips_plan {
     uint64_t kcap;
     // workspace layout (byte offsets)
     int32_t ctas;           // binning CTAs (persistent grid)
+    bool gbin = false;      // global-counter binning (T > kMaxTilesSmem, or TRIPS_FORCE_GLOBAL_BINNING)
+    size_t off_gbsum = 0;   // [ceil(T / 1024)] segment totals of the global tile scan
     size_t off_geo, off_tau, off_z, off_hist, off_cvis, off_toff, off_tcnt, off_bkey, off_borig, off_pcnt, off_pmeta, off_kept, off_kgam,
         off_own, off_kpkey, off_kpinfo, off_kpcnt, off_stats, ws_bytes;
     // state
@@ -140,7 +143,7 @@ int num_sms()
 template <int FC>
 int set_emit_attr(size_t bytes)
 {
-    return (int)cudaFuncSetAttribute(k_count<FC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    return (int)cudaFuncSetAttribute(k_count<FC, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
 // Opt the binning kernels into > 48 KB of dynamic shared memory (one counter per tile).
@@ -151,7 +154,7 @@ int set_smem_attrs(size_t bytes)
     std::lock_guard<std::mutex> lk(g_dev_mu);
     size_t& done = done_dev[dev];
     if (bytes <= done) return TRIPS_OK;
-    cudaError_t e = cudaFuncSetAttribute(k_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    cudaError_t e = cudaFuncSetAttribute(k_emit<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     int bad = (int)e;
     bad |= (int)cudaFuncSetAttribute(k_tscan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     bad |= set_emit_attr<4>(bytes) | set_emit_attr<8>(bytes) | set_emit_attr<12>(bytes) | set_emit_attr<16>(bytes) |
@@ -277,14 +280,18 @@ int trips_plan_create(const trips_config* cfg, int32_t width, int32_t height, in
     p->T = tiles;
     p->pyr_floats = pix * (F + 1);
     p->kcap = (uint64_t)tiles * kTilePix * kCap;       // kept lists: 16 slots per tile pixel
-    if (p->kcap >= (uint64_t(1) << 32) || tiles > kMaxTilesSmem) { delete p; return TRIPS_ERR_ARG; }
+    if (p->kcap >= (uint64_t(1) << 32)) { delete p; return TRIPS_ERR_ARG; }
+    // more tiles than the per-CTA shared-memory counters hold (e.g. 8K frames): global counters
+    const char* force = getenv("TRIPS_FORCE_GLOBAL_BINNING");     // tests: exercise that path at small sizes
+    p->gbin = tiles > kMaxTilesSmem || (force && force[0] == '1');
     const size_t N = (size_t)(max_points > 0 ? max_points : 1);
     size_t o = 0;
     p->ctas = num_sms() * kBinCtasPerSm;
     p->off_geo = o;    o = align256(o + N * 16);
     p->off_tau = o;    o = align256(o + N * p->FC * sizeof(float));   // used only when desc is not gatherable in place
     p->off_z = o;      o = align256(o + N * sizeof(float));
-    p->off_hist = o;   o = align256(o + (size_t)p->ctas * tiles * 4);
+    p->off_hist = o;   o = align256(o + (p->gbin ? 0 : (size_t)p->ctas * tiles * 4));
+    p->off_gbsum = o;  o = align256(o + (size_t)(tiles + 1023) / 1024 * 4);
     p->off_cvis = o;   o = align256(o + (size_t)p->ctas * 4);
     p->off_toff = o;   o = align256(o + ((size_t)tiles + 1) * 4);
     p->off_tcnt = o;   o = align256(o + (size_t)(tiles + 1) * 4);   // [T] = k_count completion ticket
@@ -362,11 +369,37 @@ int trips_project(trips_plan* p, void* ws, const trips_camera* c, int64_t n, con
     if (rc) return rc;
     rc = cuda_status(cudaMemsetAsync(P.tile_cnt, 0, (size_t)(p->T + 1) * 4, st));
     if (rc) return rc;
+    if (p->gbin) {
+        uint32_t* bsum = reinterpret_cast<uint32_t*>(static_cast<char*>(ws) + p->off_gbsum);
+        const int nseg = (p->T + 1023) / 1024;
+        {
+            StageScope sc(p, 0, st);
+            TRIPS_FC_SWITCH(p->FC, (k_count<kFC, true><<<p->ctas, kBinThreads, 0, st>>>(P, level_out, proj_out)));
+            if ((rc = check_launch())) return rc;
+        }
+        {
+            StageScope sc(p, 2, st);
+            k_gscan_seg<<<nseg, 1024, 0, st>>>(P, bsum);
+            if ((rc = check_launch())) return rc;
+            k_gscan_top<<<1, 1024, 0, st>>>(P, bsum);
+            if ((rc = check_launch())) return rc;
+            k_gscan_add<<<nseg, 1024, 0, st>>>(P, bsum);
+            if ((rc = check_launch())) return rc;
+            if ((rc = cuda_status(cudaMemsetAsync(P.tile_cnt, 0, (size_t)p->T * 4, st)))) return rc;   // -> cursors
+        }
+        {
+            StageScope sc(p, 1, st);
+            k_emit<true><<<p->ctas, kBinThreads, 0, st>>>(P);
+            if ((rc = check_launch())) return rc;
+        }
+        p->stage = 1;
+        return TRIPS_OK;
+    }
     const size_t hsm = (size_t)p->T * 4;
     if ((rc = set_smem_attrs(hsm))) return rc;
     {
         StageScope sc(p, 0, st);
-        TRIPS_FC_SWITCH(p->FC, (k_count<kFC><<<p->ctas, kBinThreads, hsm, st>>>(P, level_out, proj_out)));
+        TRIPS_FC_SWITCH(p->FC, (k_count<kFC, false><<<p->ctas, kBinThreads, hsm, st>>>(P, level_out, proj_out)));
         if ((rc = check_launch())) return rc;
     }
 #if TRIPS_TILE_SCAN == 0
@@ -378,7 +411,7 @@ int trips_project(trips_plan* p, void* ws, const trips_camera* c, int64_t n, con
 #endif
     {
         StageScope sc(p, 1, st);
-        k_emit<<<p->ctas, kBinThreads, hsm, st>>>(P);
+        k_emit<false><<<p->ctas, kBinThreads, hsm, st>>>(P);
         if ((rc = check_launch())) return rc;
     }
     p->stage = 1;

@@ -124,3 +124,15 @@ def test_no_cpu_fallback_when_library_missing(A, tmp_path, monkeypatch):
     monkeypatch.setattr(A, "LIB_PATH", str(tmp_path / "libtrips.so"))
     with pytest.raises(ImportError):
         A.lib()
+
+
+def test_large_plans_are_accepted(A):
+    """More tiles than the shared-memory binning counters hold (8K frames: 172 200 tiles at 4
+    layers) select global-counter binning instead of failing; > 2^20 tiles is rejected."""
+    plan = A.trips_plan_create(4, 4, 7680, 4320, 10)
+    try:
+        assert A.trips_pyramid_floats(plan) > 7680 * 4320 * 5
+    finally:
+        A.trips_plan_destroy(plan)
+    with pytest.raises(A.TripsError):
+        A.trips_plan_create(1, 4, 32768, 32768, 10)        # 4 194 304 tiles

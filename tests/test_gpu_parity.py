@@ -609,3 +609,29 @@ def test_coarse_full_size_c3_sampled(dev):
     check_backward(sc, got, G, mask=mask, coarse_layers=7)
     plain = gpu_run(sc, dev, export=True)
     assert np.array_equal(plain["counts"], got["counts"])          # counts stay the own lists
+
+
+def test_large_plan_global_binning(dev):
+    """A plan with more tiles than the per-CTA shared-memory counters hold (4096 x 3072, 3 layers:
+    64 512 tiles > 49 152) bins with global counters (k_count<.., true>, k_gscan_*, k_emit<true>);
+    forward + backward on sampled pixels against the oracle."""
+    import dataclasses
+    base = scenes.make_config("C2", n=300_000)
+    cam = scenes._orbit_cam(0.6, W=4096, H=3072, fx=2453.0)
+    sc = dataclasses.replace(base, cams=[cam], n_layers=3, forward_only=False)
+    mask = _sample_mask(cam, sc.n_layers, seed=9)
+    G = grads_for(sc, cam, seed=2, mask=mask)
+    got = gpu_run(sc, dev, G=G, save=True)
+    check_forward(sc, got, mask=mask)
+    check_backward(sc, got, G, mask=mask)
+
+
+def test_forced_global_binning_small_scenes(dev, monkeypatch):
+    """The global-counter binning path on the small parity scenes (forced by the plan-time switch
+    TRIPS_FORCE_GLOBAL_BINNING): bit-exact counts / kept lists, forward and backward in tolerance."""
+    monkeypatch.setenv("TRIPS_FORCE_GLOBAL_BINNING", "1")
+    for sc in (scenes.c1(), scenes.adversarial_scene(), scenes.tiny_scene(11, n=30000, F=4, W=40, H=24, n_layers=3)):
+        G = grads_for(sc, sc.cams[0], seed=4)
+        got = gpu_run(sc, dev, G=G, save=True)
+        check_forward(sc, got)
+        check_backward(sc, got, G)
