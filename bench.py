@@ -668,7 +668,7 @@ def main():
                     help="cross-rank gradient reduction of the timed step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-configs", action="store_true", help="skip the C2/C3/C5 side measurements")
-    ap.add_argument("--streams", type=int, default=3,
+    ap.add_argument("--streams", type=int, default=2,
                     help="CUDA streams (one plan + workspace each) the views of a step are spread over")
     ap.add_argument("--no-random-order", action="store_true", help="skip the random-order side measurement")
     args = ap.parse_args()
