@@ -61,6 +61,8 @@ struct Params {
     uint32_t* cta_vis;     // [C]      visible points per binning CTA (statistics)
     uint32_t* tile_cnt;    // [T]      pairs per tile (k_count's reservations)
     uint32_t* tile_off;    // [T+1]    first pair of each tile's bin; [T] = number of pairs M
+    uint32_t* tile_perm;   // [T]      launch order of the per-tile kernels: heaviest bins first
+                           //          (nullptr: tile order) -- the long tiles start in the first wave
     uint64_t* bin_key;     // [8n]     (z bits << 32 | i) per (tile, pair), tile-major
     uint16_t* bin_orig;    // [8n]     footprint origin in the tile: (qx0+1) | (qy0+1) << 5
     uint32_t* pix_cnt;     // [T*256]  list length per tile pixel

@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
     __shared__ uint32_t s_pinfo[kChunk];
 #endif
 
-    const int t = blockIdx.x;
+    const int t = P.tile_perm ? (int)__ldg(P.tile_perm + blockIdx.x) : (int)blockIdx.x;
     const TileCoord tc = tile_coord(P, t);
     const LayerGeom& G = P.L[tc.l];
     const int tid = threadIdx.x;
@@ -662,7 +662,7 @@ __device__ __forceinline__ void emit_kept_pairs(const Params& P, int t, uint32_t
 template <int FC>
 __global__ void __launch_bounds__(kTilePix) k_coarse_blend(Params P, float* __restrict__ pyramid, int save)
 {
-    const int t = blockIdx.x;
+    const int t = P.tile_perm ? (int)__ldg(P.tile_perm + blockIdx.x) : (int)blockIdx.x;
     const TileCoord tc = tile_coord(P, t);
     const LayerGeom& G = P.L[tc.l];
     const int tid = threadIdx.x;
@@ -875,7 +875,7 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_BWD_CTAS) k_backward_pairs(Par
     __shared__ float s_g[kGs ? FC * kTilePix : 1];
     __shared__ float s_c[kCap * kTilePix];           // [m][pixel] c_m, then dL/dgamma_m
     __shared__ float s_tg[kCap * kTilePix];          // [m][pixel] T_m gamma_m
-    const int t = blockIdx.x;
+    const int t = P.tile_perm ? (int)__ldg(P.tile_perm + blockIdx.x) : (int)blockIdx.x;
     const TileCoord tc = tile_coord(P, t);           // kernel parameters only: no memory round trip
     const LayerGeom& G = P.L[tc.l];
     const int tid = threadIdx.x;
@@ -1058,7 +1058,7 @@ template <int FC, bool CAM, bool SCREEN>
 __global__ void __launch_bounds__(kTilePix, FC <= 4 ? 3 : 2) k_backward_coarse(Params P, const float* __restrict__ gpyr,
                                                        GradOut go, float* __restrict__ grad_cam)
 {
-    const int t = blockIdx.x;
+    const int t = P.tile_perm ? (int)__ldg(P.tile_perm + blockIdx.x) : (int)blockIdx.x;
     const TileCoord tc = tile_coord(P, t);
     const LayerGeom& G = P.L[tc.l];
     const int tid = threadIdx.x;
@@ -1154,7 +1154,7 @@ __global__ void __launch_bounds__(kTilePix, FC <= 4 ? 3 : 2) k_backward_coarse(P
 
 __global__ void __launch_bounds__(kTilePix) k_export(Params P, int what, void* dst)
 {
-    const int t = blockIdx.x;
+    const int t = P.tile_perm ? (int)__ldg(P.tile_perm + blockIdx.x) : (int)blockIdx.x;
     const TileCoord tc = tile_coord(P, t);
     const LayerGeom& G = P.L[tc.l];
     const int tid = threadIdx.x;

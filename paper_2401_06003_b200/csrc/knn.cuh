@@ -32,6 +32,10 @@ constexpr uint64_t kKnnNonFinite = (1ull << 48) - 1;
 #ifndef TRIPS_KNN_UNION
 #define TRIPS_KNN_UNION 6          // warp mode when the union box is <= this x the largest lane box (+64 steps)
 #endif
+#ifndef TRIPS_KNN_GROUP
+#define TRIPS_KNN_GROUP 32         // lanes whose queries share one union box (power of 2; 4 / 8 / 16 measured slower)
+#endif
+constexpr int kKnnGroup = TRIPS_KNN_GROUP;
 #ifndef TRIPS_KNN_WIN
 #define TRIPS_KNN_WIN 8
 #endif
@@ -220,6 +224,8 @@ __device__ __forceinline__ uint64_t knn_bigmin(uint64_t c, uint64_t zmin, uint64
 __global__ void __launch_bounds__(256) k_knn_query(KnnWs W, float* __restrict__ size_out, int32_t* __restrict__ nbr_out)
 {
     constexpr unsigned kAll = 0xffffffffu;
+    __shared__ float4 s_stage[8][32];                // per warp: in-box points of one 32-position step
+    __shared__ int s_spos[8][32];
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
     const bool live = k < W.n;                       // no early return: the warp cooperates below
@@ -272,22 +278,27 @@ __global__ void __launch_bounds__(256) k_knn_query(KnnWs W, float* __restrict__ 
     // broadcast to every lane).  Otherwise (the warp straddles a far jump of the curve) each lane
     // scans its own box with BIGMIN jumps.  Either way every point of a lane's box is evaluated exactly once (window
     // positions skipped), so the top-4 is exact.
-    const unsigned act = __ballot_sync(kAll, need);
+    // groups of kKnnGroup lanes (consecutive sorted positions) cooperate; all sync operations use
+    // the group's mask, so the groups of a warp run independently
+    constexpr int G = kKnnGroup;
+    const int gl = lane & (G - 1), gbase = lane - gl;
+    const unsigned gmask = (G == 32) ? kAll : (((1u << G) - 1u) << gbase);
+    const unsigned act = __ballot_sync(kAll, need) & gmask;
     if (act) {
         int ulo[3], uhi[3], lext = 0, uext = 0;
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-            ulo[a] = __reduce_min_sync(kAll, need ? qlo[a] : (1 << kKnnBits));
-            uhi[a] = __reduce_max_sync(kAll, need ? qhi[a] : -1);
+            ulo[a] = __reduce_min_sync(gmask, need ? qlo[a] : (1 << kKnnBits));
+            uhi[a] = __reduce_max_sync(gmask, need ? qhi[a] : -1);
             lext = max(lext, qhi[a] - qlo[a]);
             uext = max(uext, uhi[a] - ulo[a]);
         }
-        lext = __reduce_max_sync(kAll, need ? lext : 0);
+        lext = __reduce_max_sync(gmask, need ? lext : 0);
         if (uext <= TRIPS_KNN_UNION * lext + 64) {
             // the union box is covered by <= 3 x 3 x 3 aligned octree cells of the smallest size that
             // spans it in 3; each cell is one contiguous code range of the sorted array, located by a
-            // lane of its own (parallel lower_bounds); the warp then sweeps the cells' ranges 32
-            // positions at a time, broadcasting the in-box points
+            // lane of the group (parallel lower_bounds); the group then sweeps the cells' ranges G
+            // positions at a time, broadcasting the in-box points through shared memory
             const uint64_t zmin = knn_code(ulo[0], ulo[1], ulo[2]), zmax = knn_code(uhi[0], uhi[1], uhi[2]);
             int sh = 0;
             while (sh < kKnnBits && ((uhi[0] >> sh) - (ulo[0] >> sh) > 2 || (uhi[1] >> sh) - (ulo[1] >> sh) > 2 ||
@@ -295,31 +306,50 @@ __global__ void __launch_bounds__(256) k_knn_query(KnnWs W, float* __restrict__ 
                 ++sh;
             const int nx = (uhi[0] >> sh) - (ulo[0] >> sh) + 1, ny = (uhi[1] >> sh) - (ulo[1] >> sh) + 1;
             const int ncell = nx * ny * ((uhi[2] >> sh) - (ulo[2] >> sh) + 1);
-            const int k0 = __shfl_sync(kAll, k, __ffs(act) - 1);
-            int ca = 0, cb = 0;                                      // this lane's cell: [ca, cb)
-            if (lane < ncell) {
-                const int cx = (ulo[0] >> sh) + lane % nx, cy = (ulo[1] >> sh) + (lane / nx) % ny;
-                const int cz = (ulo[2] >> sh) + lane / (nx * ny);
-                const uint64_t base = knn_code(cx << sh, cy << sh, cz << sh);
-                ca = knn_lower_bound(codes, nf, base, k0);
-                cb = knn_lower_bound(codes, nf, base + (1ull << (3 * sh)), ca < nf ? ca : nf - 1);
-                TRIPS_KNN_COUNT(2, 1);
+            const int k0 = __shfl_sync(gmask, k, __ffs(act) - 1);
+            float4* stage = s_stage[threadIdx.x >> 5] + gbase;
+            int* spos = s_spos[threadIdx.x >> 5] + gbase;
+            constexpr int kRounds = (27 + G - 1) / G;
+            int ca[kRounds], cb[kRounds];                            // this lane's cells: [ca, cb)
+#pragma unroll
+            for (int rr = 0; rr < kRounds; ++rr) {
+                ca[rr] = 0;
+                cb[rr] = 0;
+                const int c = gl + rr * G;
+                if (c < ncell) {
+                    const int cx = (ulo[0] >> sh) + c % nx, cy = (ulo[1] >> sh) + (c / nx) % ny;
+                    const int cz = (ulo[2] >> sh) + c / (nx * ny);
+                    const uint64_t base = knn_code(cx << sh, cy << sh, cz << sh);
+                    ca[rr] = knn_lower_bound(codes, nf, base, k0);
+                    cb[rr] = knn_lower_bound(codes, nf, base + (1ull << (3 * sh)), ca[rr] < nf ? ca[rr] : nf - 1);
+                    TRIPS_KNN_COUNT(2, 1);
+                }
             }
             for (int cc = 0; cc < ncell; ++cc) {
-                const int a = __shfl_sync(kAll, ca, cc), b = __shfl_sync(kAll, cb, cc);
-                for (int j = a; j < b; j += 32) {
-                    const int pos = j + lane;
+                int va = 0, vb = 0;
+#pragma unroll
+                for (int rr = 0; rr < kRounds; ++rr)
+                    if (cc / G == rr) { va = ca[rr]; vb = cb[rr]; }
+                const int a = __shfl_sync(gmask, va, gbase + cc % G), b = __shfl_sync(gmask, vb, gbase + cc % G);
+                for (int j = a; j < b; j += G) {
+                    // the in-box points of these G positions are compacted into the group's stage
+                    // and read back by every lane of the group (broadcast loads)
+                    const int pos = j + gl;
                     const bool inb = pos < b && knn_in_box(codes[pos], zmin, zmax);
-                    const float4 q = inb ? pts[pos] : make_float4(0.f, 0.f, 0.f, 0.f);
-                    unsigned m = __ballot_sync(kAll, inb);
-                    while (m) {
-                        const int bl = __ffs(m) - 1;
-                        m &= m - 1;
-                        const float qx = __shfl_sync(kAll, q.x, bl), qy = __shfl_sync(kAll, q.y, bl);
-                        const float qz = __shfl_sync(kAll, q.z, bl), qw = __shfl_sync(kAll, q.w, bl);
-                        const int pb = j + bl;
-                        if (need && pb != k && (pb < w0 || pb > w1)) cand_pt(qx, qy, qz, __float_as_uint(qw));
+                    const unsigned m = (__ballot_sync(gmask, inb) & gmask) >> gbase;
+                    if (inb) {
+                        const int slot = __popc(m & ((1u << gl) - 1u));
+                        stage[slot] = pts[pos];
+                        spos[slot] = pos;
                     }
+                    __syncwarp(gmask);
+                    const int cnt = __popc(m);
+                    for (int e = 0; e < cnt; ++e) {
+                        const float4 q = stage[e];
+                        const int pb = spos[e];
+                        if (need && pb != k && (pb < w0 || pb > w1)) cand_pt(q.x, q.y, q.z, __float_as_uint(q.w));
+                    }
+                    __syncwarp(gmask);
                 }
             }
         } else if (need) {

@@ -17,6 +17,9 @@
 #include "morton.cuh"
 #include "microbench.cuh"
 #include "decoder.cuh"
+#ifndef TRIPS_TILE_PERM
+#define TRIPS_TILE_PERM 1
+#endif
 #include <cudaTypedefs.h>
 
 using namespace trips;
@@ -47,6 +50,7 @@ struct trips_plan {
     // workspace layout (byte offsets)
     int32_t ctas;           // binning CTAs (persistent grid)
     bool gbin = false;      // global-counter binning (T > kMaxTilesSmem, or TRIPS_FORCE_GLOBAL_BINNING)
+    size_t off_tperm = 0;   // [T] heaviest-first tile order (smem binning only)
     size_t off_gbsum = 0;   // [ceil(T / 1024)] segment totals of the global tile scan
     size_t off_geo, off_tau, off_z, off_hist, off_cvis, off_toff, off_tcnt, off_bkey, off_borig, off_pcnt, off_pmeta, off_kept, off_kgam,
         off_own, off_kpkey, off_kpinfo, off_kpcnt, off_stats, ws_bytes;
@@ -191,6 +195,7 @@ Params make_params(const trips_plan* p, void* ws)
     P.cta_vis = reinterpret_cast<uint32_t*>(b + p->off_cvis);
     P.tile_off = reinterpret_cast<uint32_t*>(b + p->off_toff);
     P.tile_cnt = reinterpret_cast<uint32_t*>(b + p->off_tcnt);
+    P.tile_perm = (TRIPS_TILE_PERM && !p->gbin && TRIPS_TILE_SCAN == 2) ? reinterpret_cast<uint32_t*>(b + p->off_tperm) : nullptr;
     P.bin_key = reinterpret_cast<uint64_t*>(b + p->off_bkey);
     P.bin_orig = reinterpret_cast<uint16_t*>(b + p->off_borig);
     P.pix_cnt = reinterpret_cast<uint32_t*>(b + p->off_pcnt);
@@ -295,6 +300,7 @@ int trips_plan_create(const trips_config* cfg, int32_t width, int32_t height, in
     p->off_cvis = o;   o = align256(o + (size_t)p->ctas * 4);
     p->off_toff = o;   o = align256(o + ((size_t)tiles + 1) * 4);
     p->off_tcnt = o;   o = align256(o + (size_t)(tiles + 1) * 4);   // [T] = k_count completion ticket
+    p->off_tperm = o;  o = align256(o + (size_t)tiles * 4);
     p->off_bkey = o;   o = align256(o + 8 * N * 8);
     p->off_borig = o;  o = align256(o + 8 * N * 2);
     p->off_pcnt = o;  o = align256(o + (size_t)tiles * kTilePix * 4);
