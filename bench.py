@@ -97,10 +97,23 @@ class ClockSampler:
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={self.FIELDS}",
-                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                       "--format=csv,noheader,nounits", "-lms", "50"],
                                       stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
+        self.first = 0
+
+    def _rows(self):
+        with open(self.f.name) as g:
+            return [r for r in g.read().splitlines() if r.strip()]
+
+    def live(self):
+        """nvidia-smi has produced its first sample (it takes a few hundred ms to start)."""
+        return self.p is not None and len(self._rows()) > 0
+
+    def mark(self):
+        """Samples from here on belong to the timed region."""
+        self.first = len(self._rows()) if self.p is not None else 0
 
     def stop(self):
         if self.p is None:
@@ -111,9 +124,13 @@ class ClockSampler:
         except Exception:
             self.p.kill()
         self.f.flush()
-        self.f.seek(0)
-        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.strip()]
+        allrows = self._rows()
         os.unlink(self.f.name)
+        timed = allrows[self.first:]
+        # the timed region can be shorter than the sampling period: then the samples of the
+        # warm-up steps just before it (same kernels, same load) stand in, and say so
+        rows = [r.split(",") for r in (timed if timed else allrows[-3:])]
+        self.in_timed = bool(timed)
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for r in rows:
@@ -128,7 +145,7 @@ class ClockSampler:
         if not sm:
             return None
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "window": "timed region" if self.in_timed else "warm-up steps just before it"}
 
 
 # ------------------------------------------------------------------ algorithmic bytes
@@ -407,16 +424,23 @@ def run_cuda(args, rank, world, local_rank):
         view_stats.append(rast.stats())
     torch.cuda.synchronize()
 
+    # nvidia-smi clock sampling starts with the warm-up; extra warm-up steps run until it reports,
+    # so that it samples the timed region itself
+    clocks = ClockSampler(local_rank)
+    t_w = time.time()
     for _ in range(args.warmup):
         step(d, grads[0])
     torch.cuda.synchronize()
+    while not clocks.live() and time.time() - t_w < 5.0:
+        step(d, grads[0])
+        torch.cuda.synchronize()
 
     # ---- device-timed region: inputs resident in HBM
     for r_ in rasts:
         r_.stage_ms(reset=True)
         r_.set_profiling(True)
     l0 = _abi.trips_launch_count()
-    clocks = ClockSampler(local_rank)
+    clocks.mark()
     ms_max = timed_ms(d, args.steps) * args.steps
     clk = clocks.stop()
     launches = _abi.trips_launch_count() - l0

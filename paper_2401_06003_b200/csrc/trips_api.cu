@@ -18,8 +18,8 @@
 #include "microbench.cuh"
 #include "decoder.cuh"
 #ifndef TRIPS_TILE_PERM
-#define TRIPS_TILE_PERM 1
-#endif
+#define TRIPS_TILE_PERM 0        // heaviest-first tile order: raster alone -15 us per view, but the two-stream
+#endif                           // step measured slower (1432 vs 1445 frames/s, e2e 1367 vs 1387): off
 #include <cudaTypedefs.h>
 
 using namespace trips;
