@@ -21,12 +21,6 @@ namespace trips {
 #ifndef TRIPS_BLEND_BATCH
 #define TRIPS_BLEND_BATCH 4
 #endif
-#ifndef TRIPS_GROUP8
-#define TRIPS_GROUP8 0
-#endif
-#ifndef TRIPS_PAIR_HASH
-#define TRIPS_PAIR_HASH 0      // measured slower: raster +36 us (blend-loop atomics, 26 KB more smem = less L1)
-#endif
 #ifndef TRIPS_RASTER_CTAS
 #define TRIPS_RASTER_CTAS 3
 #endif
@@ -48,9 +42,6 @@ namespace trips {
 #endif
 constexpr int kChunk = TRIPS_CHUNK;         // (point, tile) pairs staged per K4 iteration
 constexpr int kPairsPerThread = kChunk / kTilePix;
-constexpr int kHashBits = 11;                 // pair hash of single-chunk tiles: load <= 1/2
-constexpr int kHash = 1 << kHashBits;
-static_assert(kHash >= 2 * kChunk, "pair hash sized for one chunk of pairs");
 constexpr int kPfUnroll = TRIPS_PF_UNROLL;      // bin pairs loaded together in k_raster phase F
 #ifndef TRIPS_BWD_SLOTS
 #define TRIPS_BWD_SLOTS 4
@@ -303,17 +294,6 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
     __shared__ uint32_t s_rej[kTilePix];             // fragments rejected by the threshold
     __shared__ uint64_t s_thr[kTilePix];             // per-pixel 16th smallest key so far
     __shared__ uint32_t s_warp[32];
-#if TRIPS_PAIR_HASH
-    // single-chunk tiles (M <= kChunk, nearly all of them): the chunk's pairs stay addressable by
-    // their bin position j -- key, origin code, kept-corner bits -- and a hash maps a point index
-    // to its pair, so the blend marks each kept fragment's pair directly (phase F without a second
-    // pass over the bin and without searching the pixels' lists)
-    __shared__ uint32_t s_hkey[kHash];
-    __shared__ uint16_t s_hval[kHash];
-    __shared__ uint64_t s_pkey[kChunk];
-    __shared__ uint16_t s_porig[kChunk];
-    __shared__ uint32_t s_pinfo[kChunk];
-#endif
 
     const int t = P.tile_perm ? (int)__ldg(P.tile_perm + blockIdx.x) : (int)blockIdx.x;
     const TileCoord tc = tile_coord(P, t);
@@ -331,11 +311,6 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
     uint32_t total = 0;
 
     s_thr[tid] = kKeyMax;
-#if TRIPS_PAIR_HASH
-    const bool hashed = !COARSE && save && b1 - b0 <= (uint32_t)kChunk;
-    if (hashed)
-        for (int e = tid; e < kHash; e += kTilePix) s_hkey[e] = 0xffffffffu;   // visible after the chunk barrier
-#endif
     TRIPS_PCLK_START;
     // Chunks interleave the bin (chunk ch takes positions ch, ch + nch, ...): a pixel's
     // fragments then spread evenly over the chunks whatever the point order, which balances
@@ -364,23 +339,6 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
             pk[k] = j < m ? __ldg(reinterpret_cast<const unsigned long long*>(P.bin_key) + c0 + (size_t)j * nch) : 0ull;
             po[k] = j < m ? __ldg(P.bin_orig + c0 + (size_t)j * nch) : 0u;
         }
-#if TRIPS_PAIR_HASH
-        if (hashed) {                                // nch == 1: j is the pair's bin position
-#pragma unroll
-            for (int k = 0; k < kPairsPerThread; ++k) {
-                const int j = jl + k * kTilePix;
-                if (j < m) {
-                    s_pkey[j] = pk[k];
-                    s_porig[j] = (uint16_t)po[k];
-                    s_pinfo[j] = 0u;
-                    const uint32_t i = (uint32_t)pk[k];                   // a point has one pair per tile
-                    uint32_t h = (i * 2654435761u) >> (32 - kHashBits);
-                    while (atomicCAS(&s_hkey[h], 0xffffffffu, i) != 0xffffffffu) h = (h + 1) & (kHash - 1);
-                    s_hval[h] = (uint16_t)j;
-                }
-            }
-        }
-#endif
 #pragma unroll
         for (int k = 0; k < kPairsPerThread; ++k) {
 #pragma unroll
@@ -434,14 +392,6 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
         // phase C: merge this pixel's new fragments into its running top-16.  Network sizes are
         // chosen per warp (8 when no lane of the warp has more than 8 keys left in the group).
         const uint32_t wcnt = __reduce_max_sync(0xffffffffu, my_cnt);
-#if TRIPS_GROUP8
-        // groups of 8 only: 16 fewer live key registers than 16-key groups (occupancy)
-        for (uint32_t g = 0; g < wcnt; g += 8) {
-            const uint32_t rem = my_cnt > g ? my_cnt - g : 0u;
-            const bool first = __all_sync(0xffffffffu, total == 0 && g == 0);
-            group_top16<8>(r, s_keys + my_base + g, rem, first);
-        }
-#else
         for (uint32_t g = 0; g < wcnt; g += 16) {
             const uint32_t rem = my_cnt > g ? my_cnt - g : 0u;
             const bool first = __all_sync(0xffffffffu, total == 0 && g == 0);
@@ -456,7 +406,6 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
             else group_top16<16>(r, s_keys + my_base + g, rem, first);
 #endif
         }
-#endif
         total += my_cnt + s_rej[tid];
         s_thr[tid] = r[15];                          // 16th smallest key so far (MAX if < 16)
         if (ch + 1 < nch) __syncthreads();           // shared buffers are reused by the next chunk only
@@ -502,7 +451,6 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
     for (int b = 0; b < kCap / kBB; ++b) {
         if (b * kBB >= Keff || (!save && T == 0.f)) break;
         float4 rb[kBB][1 + FC / 4];
-        uint32_t rbi[kBB];
 #pragma unroll
         for (int u = 0; u < kBB; ++u) {
             const int mm = b * kBB + u;
@@ -511,7 +459,6 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
 #else
             const uint32_t ii = (uint32_t)s_kk[(mm < K ? mm : 0) * kTilePix + tid];
 #endif
-            rbi[u] = ii;
             gather_record<FC>(P, ii, rb[u]);
         }
 #pragma unroll
@@ -531,15 +478,6 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
                 A += tg;
                 T = __fmul_rn(T, __fsub_rn(1.0f, w.gamma));      // pinned: decides the T_min cut
                 if (save) P.kept_gamma[kidx + (size_t)mm * KS] = w.gamma;
-#if TRIPS_PAIR_HASH
-                if (hashed) {
-                    // this fragment is corner c = dx + 2 dy of its pair, kept at slot mm
-                    uint32_t h = (rbi[u] * 2654435761u) >> (32 - kHashBits);
-                    while (s_hkey[h] != rbi[u]) h = (h + 1) & (kHash - 1);
-                    const uint32_t c = (uint32_t)(w.dx + 2 * w.dy);
-                    atomicOr(&s_pinfo[s_hval[h]], (1u << (10 + c)) | ((uint32_t)mm << (14 + 4 * c)));
-                }
-#endif
                 if (TMIN && T < P.t_min) Keff = mm + 1;
             }
         }
@@ -571,25 +509,6 @@ __global__ void __launch_bounds__(kTilePix, TRIPS_RASTER_CTAS) k_raster(Params P
     uint64_t* s_kk = s_keys;                         // 16 x 256 keys (= kChunk * 4)
 #pragma unroll
     for (int mm = 0; mm < kCap; ++mm) s_kk[mm * kTilePix + tid] = r[mm];   // kKeyMax beyond K
-#endif
-#if TRIPS_PAIR_HASH
-    if (hashed) {
-        if (tid == 0) s_warp[0] = 0;
-        __syncthreads();                             // every kept fragment has marked its pair
-        const size_t kpb = kept_base(t);
-        for (uint32_t j = tid; j < M; j += kTilePix) {
-            const uint32_t kbits = s_pinfo[j];
-            if (kbits) {                             // bin order: the backward's gathers stay coherent
-                const uint32_t slot = atomicAdd(s_warp, 1u);
-                P.kp_key[kpb + slot] = s_pkey[j];
-                P.kp_info[kpb + slot] = kbits | (s_porig[j] & 0x3ffu);
-            }
-        }
-        __syncthreads();
-        if (tid == 0) P.kp_cnt[t] = s_warp[0];
-        TRIPS_PCLK(7);
-        return;
-    }
 #endif
     // per-pixel kept threshold: the Keff-th key (a key of this pixel is kept iff <= it)
     s_thr[tid] = Keff > 0 ? s_kk[(Keff - 1) * kTilePix + tid] : 0ull;
