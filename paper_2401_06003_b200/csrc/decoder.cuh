@@ -496,8 +496,20 @@ __global__ void __launch_bounds__(kDecThreads, 1) k_dec_conv(const __grid_consta
                     if (x < L.W)
                         for (int oc = 0; oc < D.out_ch; ++oc) {
                             float sacc = __ldg(bo + oc);
+                            const float* w = Wo + oc * kDecHidden;
+                            if ((reinterpret_cast<uintptr_t>(w) & 15u) == 0) {     // 16-B rows: vector loads
 #pragma unroll
-                            for (int c = 0; c < 32; ++c) sacc = fmaf(__ldg(Wo + oc * kDecHidden + c), o[c], sacc);
+                                for (int c4 = 0; c4 < 8; ++c4) {
+                                    const float4 wv = __ldg(reinterpret_cast<const float4*>(w) + c4);
+                                    sacc = fmaf(wv.x, o[4 * c4], sacc);
+                                    sacc = fmaf(wv.y, o[4 * c4 + 1], sacc);
+                                    sacc = fmaf(wv.z, o[4 * c4 + 2], sacc);
+                                    sacc = fmaf(wv.w, o[4 * c4 + 3], sacc);
+                                }
+                            } else {
+#pragma unroll
+                                for (int c = 0; c < 32; ++c) sacc = fmaf(__ldg(w + c), o[c], sacc);
+                            }
                             D.out[oc * plane + p] = sacc;
                         }
                 }
