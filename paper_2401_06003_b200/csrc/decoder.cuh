@@ -186,9 +186,12 @@ __global__ void __launch_bounds__(256) k_dec_pack(DecParams D)
 // that interpolates it; then one thread per (pixel, 8-channel group) writes 16 bytes of X_l.
 constexpr int kPrepW = 32, kPrepH = 16;
 constexpr int kPrepSW = kPrepW / 2 + 2, kPrepSH = kPrepH / 2 + 2;
+template <int NG>   // 16-byte channel groups per pixel: D.xc / 8
 __global__ void __launch_bounds__(256) k_dec_prep(DecParams D, int l)
 {
     __shared__ __align__(16) float s_y[kPrepSH * kPrepSW * kDecHidden];
+    __shared__ int4 s_src[kPrepW * kPrepH];          // per output pixel: its 4 source offsets in s_y
+    __shared__ float2 s_lw[kPrepW * kPrepH];         // and its bilinear weights (lx, ly)
     const DecLayer& L = D.L[l];
     const int npx = L.H * L.W;                       // < 2^31 / 8 (checked on the host)
     const int x0 = blockIdx.x * kPrepW, y0 = blockIdx.y * kPrepH;
@@ -204,12 +207,22 @@ __global__ void __launch_bounds__(256) k_dec_prep(DecParams D, int l)
             reinterpret_cast<float4*>(s_y)[e] =
                 __ldg(reinterpret_cast<const float4*>(Yc + ((int64_t)sy * L.Wc + sx) * kDecHidden) + c4);
         }
+        // the interpolation setup once per output pixel (bilinear 2x, half-pixel centres: output i
+        // samples (i + 0.5) / 2 - 0.5 >= 0, clamped), shared by its 4 channel groups
+        for (int q = threadIdx.x; q < kPrepW * kPrepH; q += blockDim.x) {
+            const int y = y0 + q / kPrepW, x = x0 + (q & (kPrepW - 1));
+            const float sy = fmaxf((y + 0.5f) * 0.5f - 0.5f, 0.f), sx = fmaxf((x + 0.5f) * 0.5f - 0.5f, 0.f);
+            const int iy0 = min((int)sy, L.Hc - 1), ix0 = min((int)sx, L.Wc - 1);
+            const int iy1 = min(iy0 + 1, L.Hc - 1), ix1 = min(ix0 + 1, L.Wc - 1);
+            s_src[q] = make_int4(((iy0 - sy0) * kPrepSW + (ix0 - sx0)) * kDecHidden, ((iy0 - sy0) * kPrepSW + (ix1 - sx0)) * kDecHidden,
+                                 ((iy1 - sy0) * kPrepSW + (ix0 - sx0)) * kDecHidden, ((iy1 - sy0) * kPrepSW + (ix1 - sx0)) * kDecHidden);
+            s_lw[q] = make_float2(sx - (float)ix0, sy - (float)iy0);
+        }
         __syncthreads();
     }
-    const int ng = D.xc / 8;                         // 16-byte channel groups per pixel
-    for (int it = threadIdx.x; it < kPrepW * kPrepH * ng; it += blockDim.x) {
-        const int q = it / ng;
-        const int grp = it - q * ng;
+    for (int it = threadIdx.x; it < kPrepW * kPrepH * NG; it += blockDim.x) {
+        const int q = it / NG;                       // compile-time divisor
+        const int grp = it - q * NG;
         const int y = y0 + q / kPrepW, x = x0 + (q & (kPrepW - 1));
         if (y >= L.H || x >= L.W) continue;
         const int p = y * L.W + x;
@@ -219,15 +232,12 @@ __global__ void __launch_bounds__(256) k_dec_prep(DecParams D, int l)
 #pragma unroll
                 for (int j = 0; j < 8; ++j) v[j] = 0.f;
             } else {
-                // bilinear 2x, half-pixel centres: output i samples (i + 0.5) / 2 - 0.5 >= 0 (clamped)
-                const float sy = fmaxf((y + 0.5f) * 0.5f - 0.5f, 0.f), sx = fmaxf((x + 0.5f) * 0.5f - 0.5f, 0.f);
-                const int iy0 = min((int)sy, L.Hc - 1), ix0 = min((int)sx, L.Wc - 1);
-                const int iy1 = min(iy0 + 1, L.Hc - 1), ix1 = min(ix0 + 1, L.Wc - 1);
-                const float ly = sy - (float)iy0, lx = sx - (float)ix0;
-                const float4* a = reinterpret_cast<const float4*>(s_y + ((iy0 - sy0) * kPrepSW + (ix0 - sx0)) * kDecHidden + grp * 8);
-                const float4* b = reinterpret_cast<const float4*>(s_y + ((iy0 - sy0) * kPrepSW + (ix1 - sx0)) * kDecHidden + grp * 8);
-                const float4* c = reinterpret_cast<const float4*>(s_y + ((iy1 - sy0) * kPrepSW + (ix0 - sx0)) * kDecHidden + grp * 8);
-                const float4* d = reinterpret_cast<const float4*>(s_y + ((iy1 - sy0) * kPrepSW + (ix1 - sx0)) * kDecHidden + grp * 8);
+                const int4 so = s_src[q];
+                const float2 w = s_lw[q];
+                const float4* a = reinterpret_cast<const float4*>(s_y + so.x + grp * 8);
+                const float4* b = reinterpret_cast<const float4*>(s_y + so.y + grp * 8);
+                const float4* c = reinterpret_cast<const float4*>(s_y + so.z + grp * 8);
+                const float4* d = reinterpret_cast<const float4*>(s_y + so.w + grp * 8);
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     const float4 A = a[h], B = b[h], C = c[h], Dd = d[h];
@@ -235,9 +245,9 @@ __global__ void __launch_bounds__(256) k_dec_prep(DecParams D, int l)
                     const float r2[4] = {C.x, C.y, C.z, C.w}, r3[4] = {Dd.x, Dd.y, Dd.z, Dd.w};
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
-                        const float top = r0[j] * (1.f - lx) + r1[j] * lx;
-                        const float bot = r2[j] * (1.f - lx) + r3[j] * lx;
-                        v[4 * h + j] = top * (1.f - ly) + bot * ly;
+                        const float top = r0[j] * (1.f - w.x) + r1[j] * w.x;
+                        const float bot = r2[j] * (1.f - w.x) + r3[j] * w.x;
+                        v[4 * h + j] = top * (1.f - w.y) + bot * w.y;
                     }
                 }
             }
@@ -251,7 +261,7 @@ __global__ void __launch_bounds__(256) k_dec_prep(DecParams D, int l)
         __half2 h2[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) h2[j] = __floats2half2_rn(v[2 * j], v[2 * j + 1]);
-        *reinterpret_cast<uint4*>(D.X + (int64_t)p * D.xc + grp * 8) = *reinterpret_cast<uint4*>(h2);
+        *reinterpret_cast<uint4*>(D.X + (int64_t)p * (NG * 8) + grp * 8) = *reinterpret_cast<uint4*>(h2);
     }
 }
 

@@ -785,7 +785,9 @@ int trips_decode(const trips_plan* p, void* dws, const float* params, int32_t ou
     const int sms = num_sms();
     for (int l = p->n_layers - 1; l >= 0; --l) {
         const DecLayer& L = D.L[l];
-        k_dec_prep<<<dim3((L.W + kPrepW - 1) / kPrepW, (L.H + kPrepH - 1) / kPrepH), 256, 0, st>>>(D, l);
+        const dim3 pg((L.W + kPrepW - 1) / kPrepW, (L.H + kPrepH - 1) / kPrepH);
+        if (D.xc == 48) k_dec_prep<6><<<pg, 256, 0, st>>>(D, l);
+        else k_dec_prep<8><<<pg, 256, 0, st>>>(D, l);
         if ((rc = check_launch())) return rc;
         CUtensorMap tmX;
         const cuuint64_t dims[3] = {(cuuint64_t)D.xc, (cuuint64_t)L.W, (cuuint64_t)L.H};
