@@ -107,12 +107,18 @@ __device__ __forceinline__ uint64_t dec_desc(uint32_t saddr)
 // instruction descriptor, kind::f16: D f32 (bits 4-5 = 1), A = B = f16 (0), both K-major,
 // N >> 3 at bits 17-22, M >> 4 at bits 24-28
 constexpr uint32_t kDecIdesc = (1u << 4) | ((uint32_t)(kDecN >> 3) << 17) | ((uint32_t)(kDecM >> 4) << 24);
+// the bypass block (columns 64-95) is non-zero only in the centre tap: the other 8 taps issue N = 64
+#ifndef TRIPS_DEC_N64
+#define TRIPS_DEC_N64 1
+#endif
+constexpr uint32_t kDecIdesc64 = (1u << 4) | ((uint32_t)(64 >> 3) << 17) | ((uint32_t)(kDecM >> 4) << 24);
 
-__device__ __forceinline__ void dec_umma(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accumulate)
+__device__ __forceinline__ void dec_umma(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accumulate,
+                                         uint32_t idesc = kDecIdesc)
 {
     asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                  "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
-                 :: "r"(d_tmem), "l"(a), "l"(b), "r"(kDecIdesc), "r"(accumulate));
+                 :: "r"(d_tmem), "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
 }
 __device__ __forceinline__ void dec_umma_commit(uint64_t* bar)
 {
@@ -399,12 +405,16 @@ __global__ void __launch_bounds__(kDecThreads, 1) k_dec_conv(const __grid_consta
                 dec_tc_fence_after();
                 const uint32_t d = tmem + (uint32_t)(acc * kDecN);
 #pragma unroll
-                for (int t = 0; t < kDecTaps; ++t) {
-                    // tap (dy, dx): the row box of y + dy from pixel dx + 1 on (one 128-B row per pixel)
+                for (int tt = 0; tt < kDecTaps; ++tt) {
+                    // tap (dy, dx): the row box of y + dy from pixel dx + 1 on (one 128-B row per pixel).
+                    // N64: the centre tap first, over all 96 columns (it initialises the bypass block),
+                    // then the other taps over the 64 gate/feature columns only
+                    const int t = TRIPS_DEC_N64 ? (tt == 0 ? 4 : (tt <= 4 ? tt - 1 : tt)) : tt;
+                    const uint32_t idesc = (TRIPS_DEC_N64 && tt > 0) ? kDecIdesc64 : kDecIdesc;
                     const uint32_t a0 = rowa[t / 3] + 128u * (uint32_t)(t % 3), b0 = dec_smem_u32(sB + t * kDecBBytes);
 #pragma unroll
                     for (int k = 0; k < kDecXC / 16; ++k)
-                        if (16 * k < D.xc) dec_umma(d, dec_desc(a0 + 32 * k), dec_desc(b0 + 32 * k), (t | k) ? 1u : 0u);
+                        if (16 * k < D.xc) dec_umma(d, dec_desc(a0 + 32 * k), dec_desc(b0 + 32 * k), (tt | k) ? 1u : 0u, idesc);
                 }
                 dec_umma_commit(mdone + acc);                 // row slots read by this tile may be reused
                 dec_umma_commit(tfull + acc);                 // accumulator ready for the epilogue
