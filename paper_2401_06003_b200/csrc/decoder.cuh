@@ -54,7 +54,11 @@ constexpr int kDecMaxOut = 32;
 constexpr int kDecRowPix = kDecM + 2;                   // a row box: the tile's 128 pixels + 1 halo each side
 constexpr int kDecRowBytes = kDecRowPix * kDecXC * 2;   // 16640 B written by the TMA
 constexpr int kDecRowSlot = 17 * 1024;                  // slots 1024-B aligned (swizzle phase)
-constexpr int kDecRowSlots = 4;                         // rows y-1, y, y+1 in use + the next one loading
+#ifndef TRIPS_DEC_SLOTS
+#define TRIPS_DEC_SLOTS 4            // 6 (prefetch 3 rows ahead) measured 0.525 vs 0.511 ms per frame
+#endif
+constexpr int kDecRowSlots = TRIPS_DEC_SLOTS;           // rows y-1, y, y+1 in use + the next ones loading
+constexpr int kDecMdone = 4;                            // per-tile MMA-completion barriers (tile mod 4)
 constexpr int kDecSmem = TRIPS_DEC_ROWS ? 1024 + kDecTaps * kDecBBytes + kDecRowSlots * kDecRowSlot + 256
                                         : 1024 + kDecTaps * kDecBBytes + kDecStages * kDecABytes + 256;
 
@@ -291,8 +295,8 @@ __global__ void __launch_bounds__(kDecThreads, 1) k_dec_conv(const __grid_consta
     uint64_t* tfull = bars + 2 * kDecStages;                      // [2]
     uint64_t* tempty = tfull + 2;                                 // [2]
     uint64_t* bbar = tempty + 2;                                  // weights loaded
-    uint64_t* mdone = bbar + 1;                                   // [2] MMAs of tile parity p finished
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mdone + 2);
+    uint64_t* mdone = bbar + 1;                                   // [4] MMAs of tile it (mod 4) finished
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mdone + kDecMdone);
 
     const DecLayer& L = D.L[l];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -311,13 +315,25 @@ __global__ void __launch_bounds__(kDecThreads, 1) k_dec_conv(const __grid_consta
     auto tile_x0 = [&](int tile) { return (tile % xt) * kDecM; };
 #endif
 
+    // epilogue constants in shared memory (broadcast reads instead of per-element L1 loads):
+    // bf [32], bg [32], then at the finest layer Wo [out_ch][32], bo [out_ch]
+    __shared__ __align__(16) float s_epi[2 * kDecHidden + kDecMaxOut * kDecHidden + kDecMaxOut];
+    {
+        const float* Pl = D.prm + L.prm_off;
+        const int64_t wsz = (int64_t)kDecHidden * L.C * 9;
+        for (int e = threadIdx.x; e < 2 * kDecHidden; e += kDecThreads)
+            s_epi[e] = e < kDecHidden ? Pl[wsz + e] : Pl[2 * wsz + kDecHidden + (e - kDecHidden)];
+        if (l == 0)
+            for (int e = threadIdx.x; e < D.out_ch * (kDecHidden + 1); e += kDecThreads)
+                s_epi[2 * kDecHidden + e] = D.prm[D.prm_out + e];       // Wo rows then bo, as stored
+    }
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < kDecStages; ++s) { dec_mbar_init(full + s, 1); dec_mbar_init(empty + s, 1); }
         for (int a = 0; a < 2; ++a) {
             dec_mbar_init(tfull + a, 1);
             dec_mbar_init(tempty + a, kDecEpiWarps);
-            dec_mbar_init(mdone + a, 1);
         }
+        for (int a = 0; a < kDecMdone; ++a) dec_mbar_init(mdone + a, 1);
         dec_mbar_init(bbar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -337,7 +353,7 @@ __global__ void __launch_bounds__(kDecThreads, 1) k_dec_conv(const __grid_consta
             dec_mbar_expect_tx(bbar, kDecTaps * kDecBBytes);
             for (int t = 0; t < kDecTaps; ++t) dec_tma_2d(sB + t * kDecBBytes, &tmB, bbar, 0, (l * kDecTaps + t) * kDecN);
 #if TRIPS_DEC_ROWS
-            // row boxes {64 ch, 130 px, 1 row} at (x0 - 1, r) in slot r & 3; a slot is reloaded once
+            // row boxes {64 ch, 130 px, 1 row} at (x0 - 1, r) in slot (r + 1) mod kDecRowSlots; a slot is reloaded once
             // the MMAs of the last tile that read it have finished
             int skey[kDecRowSlots], slast[kDecRowSlots];
 #pragma unroll
@@ -347,12 +363,14 @@ __global__ void __launch_bounds__(kDecThreads, 1) k_dec_conv(const __grid_consta
                 const int y = tile_y(tile), x0 = tile_x0(tile);
 #pragma unroll
                 for (int dy = -1; dy <= 1; ++dy) {
-                    const int r = y + dy, sl = r & (kDecRowSlots - 1);
+                    const int r = y + dy, sl = (r + 1) % kDecRowSlots;
                     const int key = (x0 / kDecM) * (L.H + 2) + (r + 1);
                     if (skey[sl] != key) {
                         if (slast[sl] >= 0) {
-                            const int w = max(slast[sl], it - 2);       // MMAs complete in issue order
-                            dec_mbar_wait(mdone + (w & 1), (uint32_t)(w >> 1) & 1u);
+                            // MMAs complete in issue order; a barrier of tile it - 4 or later has
+                            // not wrapped (its next phase is a tile not loaded yet)
+                            const int w = max(slast[sl], it - kDecMdone);
+                            dec_mbar_wait(mdone + (w & (kDecMdone - 1)), (uint32_t)(w / kDecMdone) & 1u);
                         }
                         dec_mbar_expect_tx(full + sl, kDecRowBytes);
                         dec_tma_3d(sA + sl * kDecRowSlot, &tmX, full + sl, 0, x0 - 1, r);
@@ -393,7 +411,7 @@ __global__ void __launch_bounds__(kDecThreads, 1) k_dec_conv(const __grid_consta
                 uint32_t rowa[3];
 #pragma unroll
                 for (int dy = -1; dy <= 1; ++dy) {            // the producer's slot bookkeeping, replayed
-                    const int r = y + dy, sl = r & (kDecRowSlots - 1);
+                    const int r = y + dy, sl = (r + 1) % kDecRowSlots;
                     const int key = (x0 / kDecM) * (L.H + 2) + (r + 1);
                     if (skey[sl] != key) {
                         skey[sl] = key;
@@ -416,7 +434,7 @@ __global__ void __launch_bounds__(kDecThreads, 1) k_dec_conv(const __grid_consta
                     for (int k = 0; k < kDecXC / 16; ++k)
                         if (16 * k < D.xc) dec_umma(d, dec_desc(a0 + 32 * k), dec_desc(b0 + 32 * k), (tt | k) ? 1u : 0u, idesc);
                 }
-                dec_umma_commit(mdone + acc);                 // row slots read by this tile may be reused
+                dec_umma_commit(mdone + (it & (kDecMdone - 1)));   // row slots read by this tile may be reused
                 dec_umma_commit(tfull + acc);                 // accumulator ready for the epilogue
             }
 #else
@@ -447,10 +465,8 @@ __global__ void __launch_bounds__(kDecThreads, 1) k_dec_conv(const __grid_consta
         // ---- epilogue warps 2-9: TMEM lane quarter q = warp % 4 (tile rows 32 q ..), channel half
         // h (16 of the 32 hidden channels: f, g and bypass columns 16 h ..)
         const int q = warp & 3, h = (warp - 2) >> 2;
-        const float* P = D.prm + L.prm_off;
-        const int64_t wsz = (int64_t)kDecHidden * L.C * 9;
-        const float* bf = P + wsz + 16 * h;
-        const float* bg = P + 2 * wsz + kDecHidden + 16 * h;
+        const float* bf = s_epi + 16 * h;
+        const float* bg = s_epi + kDecHidden + 16 * h;
         const bool last = l == 0;
         float* Yo = D.Y[l & 1];
         int it = 0;
@@ -475,7 +491,7 @@ __global__ void __launch_bounds__(kDecThreads, 1) k_dec_conv(const __grid_consta
                 float o[16];
 #pragma unroll
                 for (int c = 0; c < 16; ++c)
-                    o[c] = dec_elu(__uint_as_float(f[c]) + __ldg(bf + c)) * dec_sigmoid(__uint_as_float(g[c]) + __ldg(bg + c)) +
+                    o[c] = dec_elu(__uint_as_float(f[c]) + bf[c]) * dec_sigmoid(__uint_as_float(g[c]) + bg[c]) +
                            __uint_as_float(b[c]);
                 if (x < L.W) {
                     float4* dst = reinterpret_cast<float4*>(Yo + p * kDecHidden + 16 * h);
@@ -505,30 +521,25 @@ __global__ void __launch_bounds__(kDecThreads, 1) k_dec_conv(const __grid_consta
                     float o[32];
 #pragma unroll
                     for (int c = 0; c < 16; ++c) {
-                        o[c] = dec_elu(__uint_as_float(f0[c]) + __ldg(bf0 + c)) * dec_sigmoid(__uint_as_float(g0[c]) + __ldg(bg0 + c)) +
+                        o[c] = dec_elu(__uint_as_float(f0[c]) + bf0[c]) * dec_sigmoid(__uint_as_float(g0[c]) + bg0[c]) +
                                __uint_as_float(b0[c]);
-                        o[16 + c] = dec_elu(__uint_as_float(f1[c]) + __ldg(bf0 + 16 + c)) *
-                                        dec_sigmoid(__uint_as_float(g1[c]) + __ldg(bg0 + 16 + c)) + __uint_as_float(b1[c]);
+                        o[16 + c] = dec_elu(__uint_as_float(f1[c]) + bf0[16 + c]) *
+                                        dec_sigmoid(__uint_as_float(g1[c]) + bg0[16 + c]) + __uint_as_float(b1[c]);
                     }
-                    const float* Wo = D.prm + D.prm_out;
-                    const float* bo = Wo + (int64_t)D.out_ch * kDecHidden;
+                    const float* Wo = s_epi + 2 * kDecHidden;                 // [out_ch][32] then bo
+                    const float* bo = Wo + D.out_ch * kDecHidden;
                     const int64_t plane = (int64_t)L.H * L.W;
                     if (x < L.W)
                         for (int oc = 0; oc < D.out_ch; ++oc) {
-                            float sacc = __ldg(bo + oc);
-                            const float* w = Wo + oc * kDecHidden;
-                            if ((reinterpret_cast<uintptr_t>(w) & 15u) == 0) {     // 16-B rows: vector loads
+                            float sacc = bo[oc];
+                            const float4* w = reinterpret_cast<const float4*>(Wo + oc * kDecHidden);
 #pragma unroll
-                                for (int c4 = 0; c4 < 8; ++c4) {
-                                    const float4 wv = __ldg(reinterpret_cast<const float4*>(w) + c4);
-                                    sacc = fmaf(wv.x, o[4 * c4], sacc);
-                                    sacc = fmaf(wv.y, o[4 * c4 + 1], sacc);
-                                    sacc = fmaf(wv.z, o[4 * c4 + 2], sacc);
-                                    sacc = fmaf(wv.w, o[4 * c4 + 3], sacc);
-                                }
-                            } else {
-#pragma unroll
-                                for (int c = 0; c < 32; ++c) sacc = fmaf(__ldg(w + c), o[c], sacc);
+                            for (int c4 = 0; c4 < 8; ++c4) {
+                                const float4 wv = w[c4];
+                                sacc = fmaf(wv.x, o[4 * c4], sacc);
+                                sacc = fmaf(wv.y, o[4 * c4 + 1], sacc);
+                                sacc = fmaf(wv.z, o[4 * c4 + 2], sacc);
+                                sacc = fmaf(wv.w, o[4 * c4 + 3], sacc);
                             }
                             D.out[oc * plane + p] = sacc;
                         }
