@@ -42,7 +42,13 @@ constexpr int kDecTaps = 9;
 constexpr int kDecStages = TRIPS_DEC_STAGES;    // A-tap ring depth (smem: 108 KB B + 16 KB per stage)
 constexpr int kDecABytes = kDecM * kDecXC * 2;          // 16 KB per tap
 constexpr int kDecBBytes = kDecN * kDecXC * 2;          // 12 KB per tap
-constexpr int kDecEpiWarps = 8;                         // 2 per TMEM lane quarter (16 channels each)
+#ifndef TRIPS_DEC_EPI16
+#define TRIPS_DEC_EPI16 1
+#endif
+// EPI16: 16 epilogue warps, 4 per TMEM lane quarter, each taking every 4th tile whole (32 channels,
+// in two 16-channel chunks); else 8 warps, 2 per lane quarter, 16 channels each of every tile
+constexpr int kDecEpiWarps = TRIPS_DEC_EPI16 ? 16 : 8;
+constexpr int kDecEpiPerTile = TRIPS_DEC_EPI16 ? 4 : 8;  // warps that arrive on a tile's tempty
 constexpr int kDecThreads = 64 + 32 * kDecEpiWarps;     // TMA warp, MMA warp, epilogue warps
 constexpr int kDecMaxOut = 32;
 #ifndef TRIPS_DEC_ROWS
@@ -54,6 +60,11 @@ constexpr int kDecMaxOut = 32;
 constexpr int kDecRowPix = kDecM + 2;                   // a row box: the tile's 128 pixels + 1 halo each side
 constexpr int kDecRowBytes = kDecRowPix * kDecXC * 2;   // 16640 B written by the TMA
 constexpr int kDecRowSlot = 17 * 1024;                  // slots 1024-B aligned (swizzle phase)
+#ifndef TRIPS_DEC_ACC
+#define TRIPS_DEC_ACC 4
+#endif
+constexpr int kDecAcc = TRIPS_DEC_ACC;                  // TMEM accumulators in flight (x 96 columns)
+constexpr int kDecTmemCols = kDecAcc * 96 <= 256 ? 256 : 512;
 #ifndef TRIPS_DEC_SLOTS
 #define TRIPS_DEC_SLOTS 4            // 6 (prefetch 3 rows ahead) measured 0.525 vs 0.511 ms per frame
 #endif
@@ -292,9 +303,9 @@ __global__ void __launch_bounds__(kDecThreads, 1) k_dec_conv(const __grid_consta
     uint64_t* bars = reinterpret_cast<uint64_t*>(sA + (TRIPS_DEC_ROWS ? kDecRowSlots * kDecRowSlot : kDecStages * kDecABytes));
     uint64_t* full = bars;                                        // [stages]
     uint64_t* empty = bars + kDecStages;                          // [stages]
-    uint64_t* tfull = bars + 2 * kDecStages;                      // [2]
-    uint64_t* tempty = tfull + 2;                                 // [2]
-    uint64_t* bbar = tempty + 2;                                  // weights loaded
+    uint64_t* tfull = bars + 2 * kDecStages;                      // [kDecAcc]
+    uint64_t* tempty = tfull + kDecAcc;                           // [kDecAcc]
+    uint64_t* bbar = tempty + kDecAcc;                            // weights loaded
     uint64_t* mdone = bbar + 1;                                   // [4] MMAs of tile it (mod 4) finished
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mdone + kDecMdone);
 
@@ -329,17 +340,17 @@ __global__ void __launch_bounds__(kDecThreads, 1) k_dec_conv(const __grid_consta
     }
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < kDecStages; ++s) { dec_mbar_init(full + s, 1); dec_mbar_init(empty + s, 1); }
-        for (int a = 0; a < 2; ++a) {
+        for (int a = 0; a < kDecAcc; ++a) {
             dec_mbar_init(tfull + a, 1);
-            dec_mbar_init(tempty + a, kDecEpiWarps);
+            dec_mbar_init(tempty + a, kDecEpiPerTile);
         }
         for (int a = 0; a < kDecMdone; ++a) dec_mbar_init(mdone + a, 1);
         dec_mbar_init(bbar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 1) {      // TMEM: 2 accumulators x 96 columns (256 allocated)
+    if (warp == 1) {      // TMEM: kDecAcc accumulators x 96 columns (256 or 512 allocated)
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
-                     :: "r"(dec_smem_u32(tmem_slot)), "n"(256) : "memory");
+                     :: "r"(dec_smem_u32(tmem_slot)), "n"(kDecTmemCols) : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
     dec_tc_fence_before();
@@ -404,8 +415,8 @@ __global__ void __launch_bounds__(kDecThreads, 1) k_dec_conv(const __grid_consta
             for (int q = 0; q < kDecRowSlots; ++q) { skey[q] = -1; snl[q] = 0; }
             int it = 0;
             for (int tile = tile0; tile < tile1; tile += tstep, ++it) {
-                const int acc = it & 1;
-                const uint32_t aph = (uint32_t)(it >> 1) & 1u;
+                const int acc = it % kDecAcc;
+                const uint32_t aph = (uint32_t)(it / kDecAcc) & 1u;
                 const int y = tile_y(tile), x0 = tile_x0(tile);
                 dec_mbar_wait(tempty + acc, aph ^ 1);
                 uint32_t rowa[3];
@@ -442,8 +453,8 @@ __global__ void __launch_bounds__(kDecThreads, 1) k_dec_conv(const __grid_consta
             uint32_t ph = 0;
             int it = 0;
             for (int tile = tile0; tile < tile1; tile += tstep, ++it) {
-                const int acc = it & 1;
-                const uint32_t aph = (uint32_t)(it >> 1) & 1u;
+                const int acc = it % kDecAcc;
+                const uint32_t aph = (uint32_t)(it / kDecAcc) & 1u;
                 dec_mbar_wait(tempty + acc, aph ^ 1);
                 dec_tc_fence_after();
                 const uint32_t d = tmem + (uint32_t)(acc * kDecN);
@@ -461,6 +472,71 @@ __global__ void __launch_bounds__(kDecThreads, 1) k_dec_conv(const __grid_consta
             }
 #endif
         }
+#if TRIPS_DEC_EPI16
+    } else {
+        // ---- epilogue warps 2-17: TMEM lane quarter q = warp % 4 (tile rows 32 q ..); warp slot
+        // h = (warp - 2) / 4 takes tiles it = h (mod 4) whole, so four tiles drain concurrently
+        static_assert(kDecAcc % 4 == 0, "EPI16 assigns accumulator it % 4 to warp slot it % 4");
+        const int q = warp & 3, h = (warp - 2) >> 2;
+        const bool last = l == 0;
+        float* Yo = D.Y[l & 1];
+        int it = 0;
+        for (int tile = tile0; tile < tile1; tile += tstep, ++it) {
+            if ((it & 3) != h) continue;
+            const int acc = it % kDecAcc;
+            const uint32_t aph = (uint32_t)(it / kDecAcc) & 1u;
+            dec_mbar_wait(tfull + acc, aph);
+            dec_tc_fence_after();
+            const int y = tile_y(tile), x = tile_x0(tile) + 32 * q + lane;
+            const int64_t p = (int64_t)y * L.W + x;
+            const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * kDecN);
+            float o[32];
+#pragma unroll
+            for (int hc = 0; hc < 2; ++hc) {
+                uint32_t f[16], g[16], b[16];
+                dec_tmem_ld16(ta + 16 * hc, f);
+                dec_tmem_ld16(ta + 32 + 16 * hc, g);
+                dec_tmem_ld16(ta + 64 + 16 * hc, b);
+                dec_tmem_wait();
+                if (hc == 1) {
+                    dec_tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) dec_mbar_arrive(tempty + acc);    // TMEM buffer may be refilled
+                }
+#pragma unroll
+                for (int c = 0; c < 16; ++c)
+                    o[16 * hc + c] = dec_elu(__uint_as_float(f[c]) + s_epi[16 * hc + c]) *
+                                         dec_sigmoid(__uint_as_float(g[c]) + s_epi[kDecHidden + 16 * hc + c]) +
+                                     __uint_as_float(b[c]);
+                if (!last && x < L.W) {
+                    float4* dst = reinterpret_cast<float4*>(Yo + p * kDecHidden + 16 * hc);
+#pragma unroll
+                    for (int c4 = 0; c4 < 4; ++c4)
+                        dst[c4] = make_float4(o[16 * hc + 4 * c4], o[16 * hc + 4 * c4 + 1], o[16 * hc + 4 * c4 + 2],
+                                              o[16 * hc + 4 * c4 + 3]);
+                }
+            }
+            if (last && x < L.W) {
+                const float* Wo = s_epi + 2 * kDecHidden;                 // [out_ch][32] then bo
+                const float* bo = Wo + D.out_ch * kDecHidden;
+                const int64_t plane = (int64_t)L.H * L.W;
+                for (int oc = 0; oc < D.out_ch; ++oc) {
+                    float sacc = bo[oc];
+                    const float4* w = reinterpret_cast<const float4*>(Wo + oc * kDecHidden);
+#pragma unroll
+                    for (int c4 = 0; c4 < 8; ++c4) {
+                        const float4 wv = w[c4];
+                        sacc = fmaf(wv.x, o[4 * c4], sacc);
+                        sacc = fmaf(wv.y, o[4 * c4 + 1], sacc);
+                        sacc = fmaf(wv.z, o[4 * c4 + 2], sacc);
+                        sacc = fmaf(wv.w, o[4 * c4 + 3], sacc);
+                    }
+                    D.out[oc * plane + p] = sacc;
+                }
+            }
+        }
+    }
+#else
     } else {
         // ---- epilogue warps 2-9: TMEM lane quarter q = warp % 4 (tile rows 32 q ..), channel half
         // h (16 of the 32 hidden channels: f, g and bypass columns 16 h ..)
@@ -471,8 +547,8 @@ __global__ void __launch_bounds__(kDecThreads, 1) k_dec_conv(const __grid_consta
         float* Yo = D.Y[l & 1];
         int it = 0;
         for (int tile = tile0; tile < tile1; tile += tstep, ++it) {
-            const int acc = it & 1;
-            const uint32_t aph = (uint32_t)(it >> 1) & 1u;
+            const int acc = it % kDecAcc;
+            const uint32_t aph = (uint32_t)(it / kDecAcc) & 1u;
             dec_mbar_wait(tfull + acc, aph);
             dec_tc_fence_after();
             const int y = tile_y(tile), x = tile_x0(tile) + 32 * q + lane;
@@ -547,10 +623,11 @@ __global__ void __launch_bounds__(kDecThreads, 1) k_dec_conv(const __grid_consta
             }
         }
     }
+#endif
     __syncthreads();
     if (warp == 1) {
         dec_tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "n"(256) : "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "n"(kDecTmemCols) : "memory");
     }
 }
 
