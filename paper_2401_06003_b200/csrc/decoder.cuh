@@ -207,10 +207,17 @@ __global__ void __launch_bounds__(256) k_dec_pack(DecParams D)
 // that interpolates it; then one thread per (pixel, 8-channel group) writes 16 bytes of X_l.
 constexpr int kPrepW = 32, kPrepH = 16;
 constexpr int kPrepSW = kPrepW / 2 + 2, kPrepSH = kPrepH / 2 + 2;
+#ifndef TRIPS_PREP_UNIFORM
+#define TRIPS_PREP_UNIFORM 1
+#endif
+// UNIFORM: items ordered group-major (a warp's 32 items share the channel group: no divergence
+// between the interpolated and the pyramid groups); source pixels padded to 36 floats in shared
+// memory so that the 16 distinct source pixels of a warp's float4 reads spread over the banks
+constexpr int kPrepSP = TRIPS_PREP_UNIFORM ? kDecHidden + 4 : kDecHidden;   // floats per staged pixel
 template <int NG>   // 16-byte channel groups per pixel: D.xc / 8
 __global__ void __launch_bounds__(256) k_dec_prep(DecParams D, int l)
 {
-    __shared__ __align__(16) float s_y[kPrepSH * kPrepSW * kDecHidden];
+    __shared__ __align__(16) float s_y[kPrepSH * kPrepSW * kPrepSP];
     __shared__ int4 s_src[kPrepW * kPrepH];          // per output pixel: its 4 source offsets in s_y
     __shared__ float2 s_lw[kPrepW * kPrepH];         // and its bilinear weights (lx, ly)
     const DecLayer& L = D.L[l];
@@ -225,7 +232,7 @@ __global__ void __launch_bounds__(256) k_dec_prep(DecParams D, int l)
             const int px = e >> 3;
             const int ry = px / kPrepSW, rx = px - ry * kPrepSW;
             const int sy = min(sy0 + ry, L.Hc - 1), sx = min(sx0 + rx, L.Wc - 1);
-            reinterpret_cast<float4*>(s_y)[e] =
+            reinterpret_cast<float4*>(s_y + px * kPrepSP)[c4] =
                 __ldg(reinterpret_cast<const float4*>(Yc + ((int64_t)sy * L.Wc + sx) * kDecHidden) + c4);
         }
         // the interpolation setup once per output pixel (bilinear 2x, half-pixel centres: output i
@@ -235,15 +242,20 @@ __global__ void __launch_bounds__(256) k_dec_prep(DecParams D, int l)
             const float sy = fmaxf((y + 0.5f) * 0.5f - 0.5f, 0.f), sx = fmaxf((x + 0.5f) * 0.5f - 0.5f, 0.f);
             const int iy0 = min((int)sy, L.Hc - 1), ix0 = min((int)sx, L.Wc - 1);
             const int iy1 = min(iy0 + 1, L.Hc - 1), ix1 = min(ix0 + 1, L.Wc - 1);
-            s_src[q] = make_int4(((iy0 - sy0) * kPrepSW + (ix0 - sx0)) * kDecHidden, ((iy0 - sy0) * kPrepSW + (ix1 - sx0)) * kDecHidden,
-                                 ((iy1 - sy0) * kPrepSW + (ix0 - sx0)) * kDecHidden, ((iy1 - sy0) * kPrepSW + (ix1 - sx0)) * kDecHidden);
+            s_src[q] = make_int4(((iy0 - sy0) * kPrepSW + (ix0 - sx0)) * kPrepSP, ((iy0 - sy0) * kPrepSW + (ix1 - sx0)) * kPrepSP,
+                                 ((iy1 - sy0) * kPrepSW + (ix0 - sx0)) * kPrepSP, ((iy1 - sy0) * kPrepSW + (ix1 - sx0)) * kPrepSP);
             s_lw[q] = make_float2(sx - (float)ix0, sy - (float)iy0);
         }
         __syncthreads();
     }
     for (int it = threadIdx.x; it < kPrepW * kPrepH * NG; it += blockDim.x) {
+#if TRIPS_PREP_UNIFORM
+        const int grp = it / (kPrepW * kPrepH);      // warp-uniform
+        const int q = it - grp * (kPrepW * kPrepH);
+#else
         const int q = it / NG;                       // compile-time divisor
         const int grp = it - q * NG;
+#endif
         const int y = y0 + q / kPrepW, x = x0 + (q & (kPrepW - 1));
         if (y >= L.H || x >= L.W) continue;
         const int p = y * L.W + x;
