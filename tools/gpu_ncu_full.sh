@@ -11,8 +11,8 @@ cap() {   # name, kernel regex, skip, count, command...
   ncu -i /tmp/$name.ncu-rep --page source --csv --print-source cuda,sass > gpurun_out/${name}_src.csv 2>/dev/null
   gzip -f gpurun_out/${name}_src.csv
 }
-cap r02_raster "k_raster" 1 1 python tools/prof_views.py --views 2 --order morton
-cap r02_backward "k_backward" 1 1 python tools/prof_views.py --views 2 --order morton
-cap r02_dec "k_dec_conv|k_dec_prep" 6 2 python tools/dec_time.py --iters 1
-cap r02_knn "k_knn_query" 0 1 python tools/knn_time.py
+cap r02f_raster "k_raster" 1 1 python tools/prof_views.py --views 2 --order morton
+cap r02f_backward "k_backward" 1 1 python tools/prof_views.py --views 2 --order morton
+cap r02f_dec "k_dec_conv|k_dec_prep" 6 2 python tools/dec_time.py --iters 1
+cap r02f_knn "k_knn_query" 0 1 python tools/knn_time.py
 ls -la gpurun_out/
